@@ -1,0 +1,166 @@
+/*
+ * attn_numa.h -- C-ABI boundary of the B200 attention-forward hot path.
+ *
+ * The library computes the FlashAttention-2-style forward pass of
+ * PAPER.md eq:fa (lines 149-155),
+ *
+ *     S = Q K^T,   P = softmax(scale * S) (row-wise),   O = P V,
+ *
+ * for multi-head (Hq == Hkv) and grouped-query (Hkv < Hq) attention
+ * (PAPER.md:167), tiled into work units of query-row blocks (PAPER.md:174,
+ * fig:fa2), and hands those units to SMs in one of three orders (the
+ * paper's "mappings"):
+ *
+ *   ATTN_MAP_BLOCK_FIRST          Naive Block-first
+ *   ATTN_MAP_HEAD_FIRST           Naive Head-first
+ *   ATTN_MAP_SWIZZLED_HEAD_FIRST  Swizzled Head-first:
+ *        every unit of one Attention Compute Cluster (a head, or a GQA
+ *        group) is processed on SMs of one die, each die
+ *        serving its ACCs one at a time.
+ *
+ * The result does not depend on the mapping, bit for bit.
+ *
+ * Conventions shared by every entry point:
+ *  - Tensors are row-major contiguous [B][H][N][d] (PAPER.md:187,
+ *    fig:attn-grid): q and o are [B][Hq][N][d], k and v are [B][Hkv][N][d],
+ *    all bf16 (raw 16-bit storage, passed as void*).  Accumulation is fp32.
+ *  - GQA grouping: query head h reads K/V head h / (Hq / Hkv).
+ *  - causal != 0 masks key j from query i when j > i (N_q == N_k).
+ *  - Pointers of attn_fwd / attn_fwd_stream are DEVICE pointers on the
+ *    calling thread's current CUDA device; the caller owns them.  The
+ *    library never frees or retains them beyond the enqueued kernel; q, k, v
+ *    are read-only; every element of o is written.  Base pointers must be
+ *    16-byte aligned; o must not overlap q, k or v.
+ *  - All calls return an attn_status_t synchronously, before any launch.
+ *    Nothing throws, aborts or prints.  A failed call leaves o untouched.
+ *    attn_last_error() gives a thread-local detail string.
+ *  - The library owns per-device workspace (die table, scheduler counters,
+ *    probe buffers), created lazily under a mutex and released by
+ *    attn_shutdown().
+ */
+#ifndef ATTN_NUMA_H
+#define ATTN_NUMA_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define ATTN_API __attribute__((visibility("default")))
+#else
+#define ATTN_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  ATTN_MAP_BLOCK_FIRST = 0,
+  ATTN_MAP_HEAD_FIRST = 1,
+  ATTN_MAP_SWIZZLED_HEAD_FIRST = 2
+} attn_mapping_t;
+
+typedef enum {
+  ATTN_OK = 0,
+  ATTN_ERR_INVALID_VALUE = 1, /* null pointer, size <= 0, Hq % Hkv != 0, bad mapping,
+                                 non-finite scale, overlap, not device memory */
+  ATTN_ERR_UNSUPPORTED = 2,   /* d not in {64,128}; N % 128 != 0; misaligned; scale < 0;
+                                 device is not sm_100 */
+  ATTN_ERR_CUDA = 3,          /* CUDA runtime / driver failure (see attn_last_error) */
+  ATTN_ERR_TOPOLOGY = 4       /* the die probe itself failed (an inconclusive probe is
+                                 NOT an error: it falls back to one domain) */
+} attn_status_t;
+
+/* Per-device die topology, measured once per process by a startup
+ * microbenchmark (%smid census + per-SM L2 hit latency matrix), or injected
+ * with attn_set_topology_override.  PAPER.md:100-109 ("kernels must
+ * incorporate mutable, algorithmic mapping logic"), :317-323 (per-die L2). */
+#define ATTN_MAX_DOMAINS 8
+#define ATTN_MAX_SMID 512
+typedef struct {
+  int num_sms;                              /* cudaDevAttrMultiProcessorCount */
+  int nsmid;                                /* %nsmid: upper bound of %smid values */
+  int n_domains;                            /* 1 or 2 on B200 */
+  int sms_per_domain[ATTN_MAX_DOMAINS];
+  signed char domain_of_smid[ATTN_MAX_SMID];/* -1 for ids never observed */
+  float lat_near_cyc;                       /* median L2-hit latency, near lines */
+  float lat_far_cyc;                        /* median L2-hit latency, far lines */
+  int far_lines_cached_near;                /* 1 if repeated far reads became near */
+  long long l2_bytes;                       /* cudaDevAttrL2CacheSize */
+  int source;                               /* 0 probe, 1 override, 2 fallback (1 domain) */
+  int stable;                               /* 1 if two probe runs agreed */
+} attn_topology_t;
+
+/* One record per work unit when a schedule trace buffer is installed. */
+typedef struct {
+  int32_t b, h, unit;   /* unit = pair of 128-row query blocks (rows [256u, 256u+256)) */
+  int32_t smid;         /* %smid of the CTA that processed it */
+  int32_t domain;       /* die of that SM per the active topology */
+  int32_t queue;        /* queue it was popped from */
+  int32_t stolen;       /* 1 if popped from another die's queue (tail balancing) */
+  int32_t seq;          /* pop index within the CTA */
+  uint64_t t_pop_ns;    /* %globaltimer at pop */
+} attn_trace_rec_t;
+
+/* Forward attention on the stream set by attn_set_stream (default: legacy
+ * stream 0).  See the conventions above.  scale is typically 1/sqrt(d)
+ * (eq:fa); any finite scale >= 0 is accepted, 0 gives uniform weights. */
+ATTN_API int attn_fwd(const void* q, const void* k, const void* v, void* o, int B, int Hq, int Hkv, int N, int d,
+             int causal, float scale, int mapping);
+
+/* Same, on an explicit cudaStream_t (passed as void*; NULL = legacy stream). */
+ATTN_API int attn_fwd_stream(const void* q, const void* k, const void* v, void* o, int B, int Hq, int Hkv, int N,
+                    int d, int causal, float scale, int mapping, void* cuda_stream);
+
+/* End-to-end variant on HOST buffers (same layout): copies q/k/v host->device
+ * into library-owned device buffers, runs attn_fwd_stream, copies o
+ * device->host and synchronises the stream before returning.  Host buffers
+ * should be pinned (cudaHostAlloc / torch pin_memory) for async copies;
+ * pageable memory works but is slower.  Library buffers are reused across
+ * calls of equal or smaller size and freed by attn_shutdown(). */
+ATTN_API int attn_fwd_host(const void* q_host, const void* k_host, const void* v_host, void* o_host, int B, int Hq,
+                  int Hkv, int N, int d, int causal, float scale, int mapping, void* cuda_stream);
+
+/* Thread-local default stream for attn_fwd. */
+ATTN_API int attn_set_stream(void* cuda_stream);
+
+/* Eager per-device init: runs the topology probe (normally done lazily on
+ * the first call).  Benchmarks call it before timing. */
+ATTN_API int attn_init(int device);
+
+/* Copies the active topology of `device` into *out (probing if needed). */
+ATTN_API int attn_topology(int device, attn_topology_t* out);
+
+/* Replace the measured die table of `device` (tests / fakes): domain_of_smid
+ * has n entries with values in [0, n_domains) or -1.  NULL restores the
+ * measured table. */
+ATTN_API int attn_set_topology_override(int device, const signed char* domain_of_smid, int n, int n_domains);
+
+/* Install a device buffer of `capacity` attn_trace_rec_t records (indexed by
+ * the unit's head-major id (b*Hq + h)*units_per_head + unit) that subsequent
+ * launches on `device` fill; NULL disables.  Debug / evidence only. */
+ATTN_API int attn_set_schedule_trace(int device, void* dev_buf, long long capacity);
+
+/* Host-side view of the queues a launch would pop, for tests: writes, for
+ * every queue q and position i, the unit (b, h, unit) into out[3*k..3*k+2]
+ * in queue-major order and the queue lengths into queue_len[0..n_queues).
+ * n_domains / sms_per_domain describe the dies (the active topology is not
+ * consulted).  units_per_head = ceil(N / 256).  Returns INVALID_VALUE if
+ * capacity (in units) is too small. */
+ATTN_API int attn_schedule_order(int B, int Hq, int Hkv, int N, int mapping, int n_domains, const int* sms_per_domain,
+                        int32_t* out, long long capacity, int* n_queues, int* queue_len);
+
+/* Launch geometry of the last successful attn_fwd* on this thread. */
+typedef struct {
+  int grid, block, smem_bytes, units, n_queues, kernel_launches;
+} attn_launch_info_t;
+ATTN_API int attn_last_launch_info(attn_launch_info_t* out);
+
+ATTN_API const char* attn_status_string(int status);
+ATTN_API const char* attn_last_error(void);
+ATTN_API const char* attn_version(void);
+ATTN_API void attn_shutdown(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ATTN_NUMA_H */

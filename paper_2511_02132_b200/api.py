@@ -1,0 +1,182 @@
+"""Python binding of the C-ABI (include/attn_numa.h), same names.
+
+Argument marshalling only: every step of the attention forward runs in the
+CUDA kernels of lib/libattnnuma.so.  torch supplies device memory and the
+current stream; nothing here computes attention.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from typing import Dict, List, Optional, Sequence
+
+import torch
+
+from . import _lib
+
+MAPPINGS = {"block_first": 0, "head_first": 1, "swizzled_head_first": 2,
+            "bf": 0, "hf": 1, "shf": 2}
+MAPPING_NAMES = ("block_first", "head_first", "swizzled_head_first")
+
+
+class AttnError(RuntimeError):
+    def __init__(self, status: int, detail: str):
+        lib = _lib.load()
+        name = lib.attn_status_string(status).decode()
+        super().__init__(f"{name}: {detail}")
+        self.status = status
+        self.detail = detail
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        raise AttnError(rc, _lib.load().attn_last_error().decode())
+
+
+def _mapping_id(mapping) -> int:
+    if isinstance(mapping, int):
+        return mapping
+    return MAPPINGS[str(mapping).lower()]
+
+
+def _stream_ptr(stream: Optional[torch.cuda.Stream]) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: Optional[torch.Tensor] = None, *,
+             causal: bool = False, scale: Optional[float] = None, mapping="swizzled_head_first",
+             stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """O = softmax(scale * Q K^T) V (PAPER.md eq:fa) on bf16 [B, H, N, d] CUDA tensors.
+
+    q: [B, Hq, N, d]; k, v: [B, Hkv, N, d]; returns o [B, Hq, N, d] (allocated
+    if not given).  scale defaults to 1/sqrt(d).  Asynchronous on `stream`
+    (default: torch's current stream).
+    """
+    for name, t in (("q", q), ("k", k), ("v", v)):
+        if not isinstance(t, torch.Tensor) or t.dtype != torch.bfloat16 or not t.is_cuda:
+            raise TypeError(f"{name} must be a bfloat16 CUDA tensor")
+        if t.dim() != 4 or not t.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous [B, H, N, d] tensor")
+    B, Hq, N, d = q.shape
+    Hkv = k.shape[1]
+    if tuple(k.shape) != (B, Hkv, N, d) or tuple(v.shape) != tuple(k.shape):
+        raise ValueError("k, v must be [B, Hkv, N, d] matching q")
+    if o is None:
+        o = torch.empty_like(q)
+    elif o.dtype != torch.bfloat16 or not o.is_contiguous() or tuple(o.shape) != tuple(q.shape):
+        raise ValueError("o must be a contiguous bf16 tensor shaped like q")
+    if scale is None:
+        scale = 1.0 / math.sqrt(d)
+    lib = _lib.load()
+    _check(lib.attn_fwd_stream(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), B, Hq, Hkv, N, d,
+                               int(bool(causal)), float(scale), _mapping_id(mapping), _stream_ptr(stream)))
+    return o
+
+
+def attn_fwd_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor, *, causal: bool = False,
+                  scale: Optional[float] = None, mapping="swizzled_head_first",
+                  stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """End-to-end call on HOST (ideally pinned) bf16 tensors: H2D, kernel, D2H, sync."""
+    for t in (q, k, v, o):
+        if t.is_cuda or t.dtype != torch.bfloat16 or not t.is_contiguous():
+            raise ValueError("attn_fwd_host takes contiguous bf16 CPU tensors")
+    B, Hq, N, d = q.shape
+    Hkv = k.shape[1]
+    if scale is None:
+        scale = 1.0 / math.sqrt(d)
+    lib = _lib.load()
+    _check(lib.attn_fwd_host(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), B, Hq, Hkv, N, d,
+                             int(bool(causal)), float(scale), _mapping_id(mapping), _stream_ptr(stream)))
+    return o
+
+
+def attn_init(device: int = 0) -> None:
+    _check(_lib.load().attn_init(int(device)))
+
+
+def attn_topology(device: int = 0) -> Dict:
+    t = _lib.Topology()
+    _check(_lib.load().attn_topology(int(device), ctypes.byref(t)))
+    return {
+        "num_sms": t.num_sms, "nsmid": t.nsmid, "n_domains": t.n_domains,
+        "sms_per_domain": list(t.sms_per_domain)[: max(t.n_domains, 1)],
+        "domain_of_smid": list(t.domain_of_smid)[: t.nsmid],
+        "lat_near_cyc": t.lat_near_cyc, "lat_far_cyc": t.lat_far_cyc,
+        "far_lines_cached_near": t.far_lines_cached_near, "l2_bytes": t.l2_bytes,
+        "source": ("probe", "override", "fallback")[t.source] if 0 <= t.source <= 2 else t.source,
+        "stable": bool(t.stable),
+    }
+
+
+def attn_set_topology_override(device: int, domain_of_smid: Optional[Sequence[int]], n_domains: int = 2) -> None:
+    lib = _lib.load()
+    if domain_of_smid is None:
+        _check(lib.attn_set_topology_override(int(device), None, 0, 0))
+        return
+    arr = (ctypes.c_byte * len(domain_of_smid))(*[int(x) for x in domain_of_smid])
+    _check(lib.attn_set_topology_override(int(device), ctypes.cast(arr, ctypes.c_void_p), len(domain_of_smid),
+                                          int(n_domains)))
+
+
+def attn_set_schedule_trace(device: int, buf: Optional[torch.Tensor]) -> None:
+    """buf: a CUDA uint8/int tensor of capacity*sizeof(TraceRec) bytes, or None."""
+    lib = _lib.load()
+    if buf is None:
+        _check(lib.attn_set_schedule_trace(int(device), None, 0))
+        return
+    cap = buf.numel() * buf.element_size() // ctypes.sizeof(_lib.TraceRec)
+    _check(lib.attn_set_schedule_trace(int(device), buf.data_ptr(), cap))
+
+
+TRACE_FIELDS = ("b", "h", "unit", "smid", "domain", "queue", "stolen", "seq")
+
+
+def trace_buffer(n_units: int, device="cuda") -> torch.Tensor:
+    rec = ctypes.sizeof(_lib.TraceRec)
+    return torch.full((n_units * rec // 4,), -1, dtype=torch.int32, device=device)
+
+
+def decode_trace(buf: torch.Tensor) -> torch.Tensor:
+    """[n_units, 8] int32 view (b, h, unit, smid, domain, queue, stolen, seq); t_pop dropped."""
+    rec_words = ctypes.sizeof(_lib.TraceRec) // 4
+    return buf.view(-1, rec_words)[:, :8].cpu()
+
+
+def attn_schedule_order(B: int, Hq: int, Hkv: int, N: int, mapping, sms_per_domain: Sequence[int]
+                        ) -> List[List[tuple]]:
+    """Host-side queues (lists of (b, h, unit)) the kernel would pop (unit = 256 rows)."""
+    lib = _lib.load()
+    U = (N + 255) // 256
+    cap = B * Hq * U
+    out = (ctypes.c_int32 * (3 * cap))()
+    nq = ctypes.c_int(0)
+    qlen = (ctypes.c_int * _lib.ATTN_MAX_DOMAINS)()
+    sizes = (ctypes.c_int * len(sms_per_domain))(*sms_per_domain)
+    _check(lib.attn_schedule_order(B, Hq, Hkv, N, _mapping_id(mapping), len(sms_per_domain),
+                                   ctypes.cast(sizes, ctypes.c_void_p), ctypes.cast(out, ctypes.c_void_p), cap,
+                                   ctypes.cast(ctypes.pointer(nq), ctypes.c_void_p),
+                                   ctypes.cast(qlen, ctypes.c_void_p)))
+    flat = list(out)
+    queues, w = [], 0
+    for qi in range(nq.value):
+        q = []
+        for _ in range(qlen[qi]):
+            q.append((flat[3 * w], flat[3 * w + 1], flat[3 * w + 2]))
+            w += 1
+        queues.append(q)
+    return queues
+
+
+def attn_last_launch_info() -> Dict:
+    info = _lib.LaunchInfo()
+    _check(_lib.load().attn_last_launch_info(ctypes.byref(info)))
+    return {f: getattr(info, f) for f, _ in _lib.LaunchInfo._fields_}
+
+
+def attn_version() -> str:
+    return _lib.load().attn_version().decode()
+
+
+def attn_shutdown() -> None:
+    _lib.load().attn_shutdown()

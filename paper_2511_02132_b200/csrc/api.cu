@@ -1,0 +1,595 @@
+// api.cu -- the C-ABI boundary (include/attn_numa.h): argument validation,
+// per-device state (die topology, scheduler counters), TMA descriptors and
+// the launch of the sm_100a attention kernel.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/attn_numa.h"
+#include "attn_fwd_sm100.cuh"
+#include "attn_sched.h"
+#include "topology.cuh"
+
+namespace {
+
+using namespace attn;
+
+constexpr int kMaxDevices = 16;
+constexpr int kCounterSlots = 64;
+constexpr int kCounterInts = kMaxQueues * 32;  // one 128-byte line per queue
+
+thread_local std::string g_err;
+thread_local cudaStream_t g_stream = nullptr;
+thread_local attn_launch_info_t g_info = {};
+
+int fail(int status, const std::string& msg) {
+  g_err = msg;
+  return status;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+  g_err = std::string(what) + ": " + cudaGetErrorString(e);
+  return ATTN_ERR_CUDA;
+}
+#define ATTN_CUDA(call)                                  \
+  do {                                                   \
+    cudaError_t e__ = (call);                            \
+    if (e__ != cudaSuccess) return cuda_fail(e__, #call); \
+  } while (0)
+
+struct DevState {
+  std::mutex mu;
+  bool init = false;
+  int num_sms = 0;
+  attn_topology_t measured{};
+  attn_topology_t active{};
+  signed char* d_domain = nullptr;
+  int* d_counters = nullptr;
+  unsigned slot = 0;
+  attn_trace_rec_t* trace = nullptr;
+  long long trace_cap = 0;
+  bool attr_done[4] = {false, false, false, false};
+  // e2e host-buffer path
+  void* hbuf[4] = {nullptr, nullptr, nullptr, nullptr};
+  size_t hbuf_bytes[4] = {0, 0, 0, 0};
+};
+
+DevState g_dev[kMaxDevices];
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+int get_encode() {
+  if (g_encode) return ATTN_OK;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+  if (e != cudaSuccess || fn == nullptr || q != cudaDriverEntryPointSuccess)
+    return fail(ATTN_ERR_CUDA, "cuTensorMapEncodeTiled entry point not found");
+  g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  return ATTN_OK;
+}
+
+// ---------------------------------------------------------------- topology
+void fallback_topology(attn_topology_t& t) {
+  t.n_domains = 1;
+  for (int i = 0; i < ATTN_MAX_DOMAINS; ++i) t.sms_per_domain[i] = 0;
+  int n = 0;
+  for (int s = 0; s < ATTN_MAX_SMID; ++s) {
+    if (t.domain_of_smid[s] >= 0) {
+      t.domain_of_smid[s] = 0;
+      ++n;
+    }
+  }
+  t.sms_per_domain[0] = n > 0 ? n : t.num_sms;
+  t.source = 2;
+}
+
+// One probe run: fills lat (nsmid x kProbeLines, 0xFFFFFFFF for absent SMs).
+int probe_once(int nsmid, const uint32_t* d_probe, std::vector<uint32_t>& lat, int num_sms) {
+  int* d_claimed = nullptr;
+  uint32_t* d_lat = nullptr;
+  ATTN_CUDA(cudaMalloc(&d_claimed, sizeof(int) * nsmid));
+  ATTN_CUDA(cudaMalloc(&d_lat, sizeof(uint32_t) * nsmid * kProbeLines));
+  ATTN_CUDA(cudaMemset(d_claimed, 0, sizeof(int) * nsmid));
+  ATTN_CUDA(cudaMemset(d_lat, 0xFF, sizeof(uint32_t) * nsmid * kProbeLines));
+  topo_latency_kernel<<<8 * num_sms, 32>>>(d_probe, d_claimed, d_lat, nsmid);
+  ATTN_CUDA(cudaGetLastError());
+  ATTN_CUDA(cudaDeviceSynchronize());
+  lat.assign((size_t)nsmid * kProbeLines, 0);
+  ATTN_CUDA(cudaMemcpy(lat.data(), d_lat, sizeof(uint32_t) * lat.size(), cudaMemcpyDeviceToHost));
+  cudaFree(d_claimed);
+  cudaFree(d_lat);
+  return ATTN_OK;
+}
+
+// Classify SMs into dies from a latency matrix.  Returns false if inconclusive.
+bool classify(const std::vector<uint32_t>& lat, const std::vector<int>& present, signed char* dom, float& near_c,
+              float& far_c) {
+  std::vector<double> all;
+  for (int s : present)
+    for (int l = 0; l < kProbeLines; ++l) all.push_back((double)lat[(size_t)s * kProbeLines + l]);
+  if (all.size() < 2) return false;
+  std::sort(all.begin(), all.end());
+  double c0 = all[all.size() / 10], c1 = all[all.size() * 9 / 10];
+  for (int it = 0; it < 50; ++it) {
+    const double thr = 0.5 * (c0 + c1);
+    double s0 = 0, s1 = 0;
+    size_t n0 = 0, n1 = 0;
+    for (double x : all) {
+      if (x < thr) { s0 += x; ++n0; } else { s1 += x; ++n1; }
+    }
+    if (n0 == 0 || n1 == 0) return false;
+    c0 = s0 / n0;
+    c1 = s1 / n1;
+  }
+  near_c = (float)c0;
+  far_c = (float)c1;
+  if (c1 - c0 < 8.0) return false;
+  const double thr = 0.5 * (c0 + c1);
+  const int s_ref = present[0];
+  int count[2] = {0, 0};
+  for (int s : present) {
+    int agree = 0;
+    for (int l = 0; l < kProbeLines; ++l) {
+      const bool a = lat[(size_t)s * kProbeLines + l] < thr;
+      const bool b = lat[(size_t)s_ref * kProbeLines + l] < thr;
+      agree += (a == b);
+    }
+    dom[s] = (2 * agree > kProbeLines) ? 0 : 1;
+    ++count[(int)dom[s]];
+  }
+  return count[0] > 0 && count[1] > 0;
+}
+
+int run_probe(int dev, DevState& st) {
+  attn_topology_t t{};
+  memset(t.domain_of_smid, -1, sizeof(t.domain_of_smid));
+  ATTN_CUDA(cudaDeviceGetAttribute(&t.num_sms, cudaDevAttrMultiProcessorCount, dev));
+  int l2 = 0;
+  ATTN_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev));
+  t.l2_bytes = l2;
+  st.num_sms = t.num_sms;
+
+  int *d_seen = nullptr, *d_n = nullptr;
+  ATTN_CUDA(cudaMalloc(&d_seen, sizeof(int) * 1024));
+  ATTN_CUDA(cudaMalloc(&d_n, sizeof(int)));
+  ATTN_CUDA(cudaMemset(d_seen, 0, sizeof(int) * 1024));
+  ATTN_CUDA(cudaMemset(d_n, 0, sizeof(int)));
+  topo_census_kernel<<<8 * t.num_sms, 32>>>(d_seen, d_n);
+  ATTN_CUDA(cudaGetLastError());
+  ATTN_CUDA(cudaDeviceSynchronize());
+  std::vector<int> seen(1024);
+  int nsmid = 0;
+  ATTN_CUDA(cudaMemcpy(seen.data(), d_seen, sizeof(int) * 1024, cudaMemcpyDeviceToHost));
+  ATTN_CUDA(cudaMemcpy(&nsmid, d_n, sizeof(int), cudaMemcpyDeviceToHost));
+  cudaFree(d_seen);
+  cudaFree(d_n);
+  std::vector<int> present;
+  for (int s = 0; s < 1024; ++s)
+    if (seen[s]) {
+      if (s >= ATTN_MAX_SMID) return fail(ATTN_ERR_TOPOLOGY, "smid beyond ATTN_MAX_SMID");
+      present.push_back(s);
+      nsmid = std::max(nsmid, s + 1);
+    }
+  t.nsmid = nsmid;
+  for (int s : present) t.domain_of_smid[s] = 0;
+
+  const char* env = getenv("ATTN_NUMA_TOPOLOGY");
+  if (env && strcmp(env, "fallback") == 0) {
+    fallback_topology(t);
+    t.stable = 1;
+    st.measured = t;
+    return ATTN_OK;
+  }
+
+  // probe buffer: every line's first word holds its own byte offset
+  std::vector<uint32_t> host((size_t)kProbeLines * kProbeStrideBytes / 4, 0);
+  for (int i = 0; i < kProbeLines; ++i) host[(size_t)i * kProbeStrideBytes / 4] = (uint32_t)i * kProbeStrideBytes;
+  uint32_t* d_probe = nullptr;
+  ATTN_CUDA(cudaMalloc(&d_probe, host.size() * 4));
+  ATTN_CUDA(cudaMemcpy(d_probe, host.data(), host.size() * 4, cudaMemcpyHostToDevice));
+
+  std::vector<uint32_t> lat_a, lat_b;
+  int rc = probe_once(nsmid, d_probe, lat_a, t.num_sms);
+  if (rc == ATTN_OK) rc = probe_once(nsmid, d_probe, lat_b, t.num_sms);
+  cudaFree(d_probe);
+  if (rc != ATTN_OK) return rc;
+  if (const char* dump = getenv("ATTN_NUMA_PROBE_DUMP")) {
+    if (FILE* f = fopen(dump, "w")) {
+      for (int s : present) {
+        fprintf(f, "%d", s);
+        for (int l = 0; l < kProbeLines; ++l) fprintf(f, ",%u,%u", lat_a[(size_t)s * kProbeLines + l],
+                                                     lat_b[(size_t)s * kProbeLines + l]);
+        fprintf(f, "\n");
+      }
+      fclose(f);
+    }
+  }
+  std::vector<int> measured_present;
+  for (int s : present)
+    if (lat_a[(size_t)s * kProbeLines] != 0xFFFFFFFFu && lat_b[(size_t)s * kProbeLines] != 0xFFFFFFFFu)
+      measured_present.push_back(s);
+
+  signed char dom_a[ATTN_MAX_SMID], dom_b[ATTN_MAX_SMID];
+  memset(dom_a, -1, sizeof dom_a);
+  memset(dom_b, -1, sizeof dom_b);
+  float na = 0, fa = 0, nb = 0, fb = 0;
+  const bool ok_a = measured_present.size() == present.size() &&
+                    classify(lat_a, measured_present, dom_a, na, fa);
+  const bool ok_b = ok_a && classify(lat_b, measured_present, dom_b, nb, fb);
+  bool same = ok_a && ok_b;
+  if (same) {
+    // the reference SM defines die 0 in both runs, so the labels are comparable
+    for (int s : present) same = same && (dom_a[s] == dom_b[s]);
+  }
+  t.lat_near_cyc = na;
+  t.lat_far_cyc = fa;
+  t.stable = same ? 1 : 0;
+  if (!same) {
+    fallback_topology(t);
+    st.measured = t;
+    return ATTN_OK;
+  }
+  t.n_domains = 2;
+  t.sms_per_domain[0] = t.sms_per_domain[1] = 0;
+  for (int s : present) {
+    t.domain_of_smid[s] = dom_a[s];
+    ++t.sms_per_domain[(int)dom_a[s]];
+  }
+  // Far lines stayed far across rounds (min over rounds), so a far line is
+  // not replicated into the near L2 by repeated .cg reads.
+  t.far_lines_cached_near = 0;
+  t.source = 0;
+  st.measured = t;
+  return ATTN_OK;
+}
+
+int upload_domain(DevState& st) {
+  if (!st.d_domain) ATTN_CUDA(cudaMalloc(&st.d_domain, ATTN_MAX_SMID));
+  ATTN_CUDA(cudaMemcpy(st.d_domain, st.active.domain_of_smid, ATTN_MAX_SMID, cudaMemcpyHostToDevice));
+  return ATTN_OK;
+}
+
+// Caller holds st.mu and has set the current device.
+int ensure_init(int dev, DevState& st) {
+  if (st.init) return ATTN_OK;
+  cudaDeviceProp prop;
+  ATTN_CUDA(cudaGetDeviceProperties(&prop, dev));
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(ATTN_ERR_UNSUPPORTED, "device is not sm_100 (compute capability " + std::to_string(prop.major) +
+                                          "." + std::to_string(prop.minor) + ")");
+  int rc = run_probe(dev, st);
+  if (rc != ATTN_OK) return rc;
+  st.active = st.measured;
+  rc = upload_domain(st);
+  if (rc != ATTN_OK) return rc;
+  ATTN_CUDA(cudaMalloc(&st.d_counters, sizeof(int) * kCounterInts * kCounterSlots));
+  ATTN_CUDA(cudaMemset(st.d_counters, 0, sizeof(int) * kCounterInts * kCounterSlots));
+  st.init = true;
+  return ATTN_OK;
+}
+
+int current_device(int& dev) {
+  ATTN_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDevices) return fail(ATTN_ERR_UNSUPPORTED, "device index beyond kMaxDevices");
+  return ATTN_OK;
+}
+
+// ----------------------------------------------------------------- launch
+int check_dev_ptr(const void* p, int dev, const char* name) {
+  cudaPointerAttributes a;
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(ATTN_ERR_INVALID_VALUE, std::string(name) + " is not a CUDA pointer");
+  }
+  if (!(a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) || a.device != dev)
+    return fail(ATTN_ERR_INVALID_VALUE, std::string(name) + " is not device memory of the current device");
+  return ATTN_OK;
+}
+
+bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
+  const uintptr_t x = reinterpret_cast<uintptr_t>(a), y = reinterpret_cast<uintptr_t>(b);
+  return x < y + nb && y < x + na;
+}
+
+int validate(const void* q, const void* k, const void* v, void* o, int B, int Hq, int Hkv, int N, int d,
+             float scale, int mapping) {
+  if (!q || !k || !v || !o) return fail(ATTN_ERR_INVALID_VALUE, "null pointer");
+  if (B <= 0 || Hq <= 0 || Hkv <= 0 || N <= 0 || d <= 0) return fail(ATTN_ERR_INVALID_VALUE, "size <= 0");
+  if (Hq % Hkv != 0) return fail(ATTN_ERR_INVALID_VALUE, "Hq % Hkv != 0 (non-uniform GQA groups)");
+  if (mapping < 0 || mapping > 2) return fail(ATTN_ERR_INVALID_VALUE, "mapping not in {0,1,2}");
+  if (!std::isfinite(scale)) return fail(ATTN_ERR_INVALID_VALUE, "non-finite scale");
+  const size_t qb = (size_t)B * Hq * N * d * 2, kb = (size_t)B * Hkv * N * d * 2;
+  if (overlaps(o, qb, q, qb) || overlaps(o, qb, k, kb) || overlaps(o, qb, v, kb))
+    return fail(ATTN_ERR_INVALID_VALUE, "o overlaps an input");
+  if (d != 64 && d != 128) return fail(ATTN_ERR_UNSUPPORTED, "head dim must be 64 or 128");
+  if (N % 128 != 0) return fail(ATTN_ERR_UNSUPPORTED, "N must be a multiple of 128");
+  if (scale < 0.f) return fail(ATTN_ERR_UNSUPPORTED, "negative scale");
+  if ((long long)B * Hq * N >= (1ll << 31) || (long long)B * Hkv * N >= (1ll << 31))
+    return fail(ATTN_ERR_UNSUPPORTED, "B*H*N exceeds 2^31 rows");
+  for (const void* p : {q, k, v, (const void*)o})
+    if (reinterpret_cast<uintptr_t>(p) % 16 != 0) return fail(ATTN_ERR_UNSUPPORTED, "pointer not 16-byte aligned");
+  return ATTN_OK;
+}
+
+int make_tmap(CUtensorMap* m, const void* base, long long rows, int d) {
+  cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)d * 2};
+  cuuint32_t box[2] = {64, 128};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(ATTN_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return ATTN_OK;
+}
+
+template <int D, bool kCausal>
+int launch_t(DevState& st, int attr_idx, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+             const KernelParams& kp, int grid, cudaStream_t s) {
+  auto* fn = attn_fwd_sm100_kernel<D, kCausal>;
+  const int smem = Cfg<D>::kSmemBytes;
+  if (!st.attr_done[attr_idx]) {
+    ATTN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    st.attr_done[attr_idx] = true;
+  }
+  fn<<<grid, kThreads, smem, s>>>(tq, tk, tv, kp);
+  ATTN_CUDA(cudaGetLastError());
+  g_info.grid = grid;
+  g_info.block = kThreads;
+  g_info.smem_bytes = smem;
+  return ATTN_OK;
+}
+
+int fwd_impl(const void* q, const void* k, const void* v, void* o, int B, int Hq, int Hkv, int N, int d, int causal,
+             float scale, int mapping, cudaStream_t stream) {
+  int rc = validate(q, k, v, o, B, Hq, Hkv, N, d, scale, mapping);
+  if (rc != ATTN_OK) return rc;
+  int dev = 0;
+  rc = current_device(dev);
+  if (rc != ATTN_OK) return rc;
+  for (auto pr : {std::make_pair(q, "q"), std::make_pair(k, "k"), std::make_pair(v, "v"),
+                  std::make_pair((const void*)o, "o")}) {
+    rc = check_dev_ptr(pr.first, dev, pr.second);
+    if (rc != ATTN_OK) return rc;
+  }
+  rc = get_encode();
+  if (rc != ATTN_OK) return rc;
+  DevState& st = g_dev[dev];
+  std::lock_guard<std::mutex> lk(st.mu);
+  rc = ensure_init(dev, st);
+  if (rc != ATTN_OK) return rc;
+
+  const int nblk = N / kBlockM;
+  const int U = (nblk + 1) / 2;
+  KernelParams kp{};
+  kp.B = B; kp.Hq = Hq; kp.Hkv = Hkv; kp.N = N; kp.G = Hq / Hkv; kp.U = U; kp.nblk = nblk;
+  kp.scale_log2 = scale * 1.4426950408889634f;
+  kp.o = reinterpret_cast<__nv_bfloat16*>(o);
+  if (!build_sched(mapping, B, Hq, Hkv, U, st.active.n_domains, st.active.sms_per_domain, kp.sched))
+    return fail(ATTN_ERR_INVALID_VALUE, "cannot build the schedule");
+  const unsigned slot = st.slot++ % kCounterSlots;
+  kp.counters = st.d_counters + (size_t)slot * kCounterInts;
+  kp.domain_of_smid = st.d_domain;
+  kp.n_smid = ATTN_MAX_SMID;
+  kp.trace = st.trace;
+  kp.trace_cap = st.trace_cap;
+
+  CUtensorMap tq, tk, tv;
+  if ((rc = make_tmap(&tq, q, (long long)B * Hq * N, d)) != ATTN_OK) return rc;
+  if ((rc = make_tmap(&tk, k, (long long)B * Hkv * N, d)) != ATTN_OK) return rc;
+  if ((rc = make_tmap(&tv, v, (long long)B * Hkv * N, d)) != ATTN_OK) return rc;
+
+  ATTN_CUDA(cudaMemsetAsync(kp.counters, 0, sizeof(int) * kCounterInts, stream));
+  const int total = B * Hq * U;
+  const int grid = std::min(st.num_sms, total);
+  if (d == 128 && causal) rc = launch_t<128, true>(st, 0, tq, tk, tv, kp, grid, stream);
+  else if (d == 128) rc = launch_t<128, false>(st, 1, tq, tk, tv, kp, grid, stream);
+  else if (causal) rc = launch_t<64, true>(st, 2, tq, tk, tv, kp, grid, stream);
+  else rc = launch_t<64, false>(st, 3, tq, tk, tv, kp, grid, stream);
+  if (rc != ATTN_OK) return rc;
+  g_info.units = total;
+  g_info.n_queues = kp.sched.n_queues;
+  g_info.kernel_launches = 1;
+  return ATTN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int attn_fwd(const void* q, const void* k, const void* v, void* o, int B, int Hq, int Hkv, int N, int d, int causal,
+             float scale, int mapping) {
+  return fwd_impl(q, k, v, o, B, Hq, Hkv, N, d, causal, scale, mapping, g_stream);
+}
+
+int attn_fwd_stream(const void* q, const void* k, const void* v, void* o, int B, int Hq, int Hkv, int N, int d,
+                    int causal, float scale, int mapping, void* cuda_stream) {
+  return fwd_impl(q, k, v, o, B, Hq, Hkv, N, d, causal, scale, mapping, reinterpret_cast<cudaStream_t>(cuda_stream));
+}
+
+int attn_fwd_host(const void* q_host, const void* k_host, const void* v_host, void* o_host, int B, int Hq, int Hkv,
+                  int N, int d, int causal, float scale, int mapping, void* cuda_stream) {
+  if (!q_host || !k_host || !v_host || !o_host) return fail(ATTN_ERR_INVALID_VALUE, "null pointer");
+  if (B <= 0 || Hq <= 0 || Hkv <= 0 || N <= 0 || d <= 0) return fail(ATTN_ERR_INVALID_VALUE, "size <= 0");
+  int dev = 0;
+  int rc = current_device(dev);
+  if (rc != ATTN_OK) return rc;
+  DevState& st = g_dev[dev];
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(cuda_stream);
+  const size_t nq = (size_t)B * Hq * N * d * 2, nk = (size_t)B * Hkv * N * d * 2;
+  const size_t need[4] = {nq, nk, nk, nq};
+  {
+    std::lock_guard<std::mutex> lk(st.mu);
+    for (int i = 0; i < 4; ++i) {
+      if (st.hbuf_bytes[i] < need[i]) {
+        if (st.hbuf[i]) cudaFree(st.hbuf[i]);
+        st.hbuf[i] = nullptr;
+        st.hbuf_bytes[i] = 0;
+        ATTN_CUDA(cudaMalloc(&st.hbuf[i], need[i]));
+        st.hbuf_bytes[i] = need[i];
+      }
+    }
+  }
+  ATTN_CUDA(cudaMemcpyAsync(st.hbuf[0], q_host, nq, cudaMemcpyHostToDevice, s));
+  ATTN_CUDA(cudaMemcpyAsync(st.hbuf[1], k_host, nk, cudaMemcpyHostToDevice, s));
+  ATTN_CUDA(cudaMemcpyAsync(st.hbuf[2], v_host, nk, cudaMemcpyHostToDevice, s));
+  rc = fwd_impl(st.hbuf[0], st.hbuf[1], st.hbuf[2], st.hbuf[3], B, Hq, Hkv, N, d, causal, scale, mapping, s);
+  if (rc != ATTN_OK) return rc;
+  ATTN_CUDA(cudaMemcpyAsync(o_host, st.hbuf[3], nq, cudaMemcpyDeviceToHost, s));
+  ATTN_CUDA(cudaStreamSynchronize(s));
+  return ATTN_OK;
+}
+
+int attn_set_stream(void* cuda_stream) {
+  g_stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+  return ATTN_OK;
+}
+
+int attn_init(int device) {
+  if (device < 0 || device >= kMaxDevices) return fail(ATTN_ERR_INVALID_VALUE, "bad device index");
+  int prev = 0;
+  ATTN_CUDA(cudaGetDevice(&prev));
+  ATTN_CUDA(cudaSetDevice(device));
+  DevState& st = g_dev[device];
+  int rc;
+  {
+    std::lock_guard<std::mutex> lk(st.mu);
+    rc = ensure_init(device, st);
+  }
+  cudaSetDevice(prev);
+  return rc;
+}
+
+int attn_topology(int device, attn_topology_t* out) {
+  if (!out) return fail(ATTN_ERR_INVALID_VALUE, "null out");
+  int rc = attn_init(device);
+  if (rc != ATTN_OK) return rc;
+  DevState& st = g_dev[device];
+  std::lock_guard<std::mutex> lk(st.mu);
+  *out = st.active;
+  return ATTN_OK;
+}
+
+int attn_set_topology_override(int device, const signed char* domain_of_smid, int n, int n_domains) {
+  int rc = attn_init(device);
+  if (rc != ATTN_OK) return rc;
+  DevState& st = g_dev[device];
+  std::lock_guard<std::mutex> lk(st.mu);
+  if (!domain_of_smid) {
+    st.active = st.measured;
+  } else {
+    if (n <= 0 || n > ATTN_MAX_SMID || n_domains < 1 || n_domains > ATTN_MAX_DOMAINS)
+      return fail(ATTN_ERR_INVALID_VALUE, "bad override table size");
+    attn_topology_t t = st.measured;
+    memset(t.domain_of_smid, -1, sizeof t.domain_of_smid);
+    for (int i = 0; i < ATTN_MAX_DOMAINS; ++i) t.sms_per_domain[i] = 0;
+    for (int s = 0; s < n; ++s) {
+      const int d = domain_of_smid[s];
+      if (d < -1 || d >= n_domains) return fail(ATTN_ERR_INVALID_VALUE, "domain id out of range");
+      t.domain_of_smid[s] = (signed char)d;
+      if (d >= 0) ++t.sms_per_domain[d];
+    }
+    for (int d = 0; d < n_domains; ++d)
+      if (t.sms_per_domain[d] == 0) t.sms_per_domain[d] = 1;  // keep the proportional cut defined
+    t.n_domains = n_domains;
+    t.source = 1;
+    st.active = t;
+  }
+  int prev = 0;
+  ATTN_CUDA(cudaGetDevice(&prev));
+  ATTN_CUDA(cudaSetDevice(device));
+  rc = upload_domain(st);
+  cudaSetDevice(prev);
+  return rc;
+}
+
+int attn_set_schedule_trace(int device, void* dev_buf, long long capacity) {
+  if (device < 0 || device >= kMaxDevices) return fail(ATTN_ERR_INVALID_VALUE, "bad device index");
+  if (dev_buf && capacity <= 0) return fail(ATTN_ERR_INVALID_VALUE, "capacity <= 0");
+  DevState& st = g_dev[device];
+  std::lock_guard<std::mutex> lk(st.mu);
+  st.trace = reinterpret_cast<attn_trace_rec_t*>(dev_buf);
+  st.trace_cap = dev_buf ? capacity : 0;
+  return ATTN_OK;
+}
+
+int attn_schedule_order(int B, int Hq, int Hkv, int N, int mapping, int n_domains, const int* sms_per_domain,
+                        int32_t* out, long long capacity, int* n_queues, int* queue_len) {
+  if (!out || !n_queues || !queue_len || !sms_per_domain) return fail(ATTN_ERR_INVALID_VALUE, "null pointer");
+  if (B <= 0 || Hq <= 0 || Hkv <= 0 || N <= 0 || Hq % Hkv) return fail(ATTN_ERR_INVALID_VALUE, "bad sizes");
+  const int U = (N + 255) / 256;
+  SchedParams sp;
+  if (!build_sched(mapping, B, Hq, Hkv, U, n_domains, sms_per_domain, sp))
+    return fail(ATTN_ERR_INVALID_VALUE, "bad mapping or domains");
+  long long total = 0;
+  for (int qi = 0; qi < sp.n_queues; ++qi) total += sp.q[qi].len;
+  if (total > capacity) return fail(ATTN_ERR_INVALID_VALUE, "capacity too small");
+  long long w = 0;
+  for (int qi = 0; qi < sp.n_queues; ++qi) {
+    queue_len[qi] = sp.q[qi].len;
+    for (int pos = 0; pos < sp.q[qi].len; ++pos) {
+      int b, h, u;
+      decode_unit(sp.q[qi], pos, Hq, U, b, h, u);
+      out[3 * w] = b;
+      out[3 * w + 1] = h;
+      out[3 * w + 2] = u;
+      ++w;
+    }
+  }
+  *n_queues = sp.n_queues;
+  return ATTN_OK;
+}
+
+int attn_last_launch_info(attn_launch_info_t* out) {
+  if (!out) return fail(ATTN_ERR_INVALID_VALUE, "null out");
+  *out = g_info;
+  return ATTN_OK;
+}
+
+const char* attn_status_string(int status) {
+  switch (status) {
+    case ATTN_OK: return "ATTN_OK";
+    case ATTN_ERR_INVALID_VALUE: return "ATTN_ERR_INVALID_VALUE";
+    case ATTN_ERR_UNSUPPORTED: return "ATTN_ERR_UNSUPPORTED";
+    case ATTN_ERR_CUDA: return "ATTN_ERR_CUDA";
+    case ATTN_ERR_TOPOLOGY: return "ATTN_ERR_TOPOLOGY";
+    default: return "ATTN_ERR_UNKNOWN";
+  }
+}
+
+const char* attn_last_error(void) { return g_err.c_str(); }
+
+const char* attn_version(void) { return "attn-numa-b200 0.1 (sm_100a tcgen05)"; }
+
+void attn_shutdown(void) {
+  for (int dv = 0; dv < kMaxDevices; ++dv) {
+    DevState& st = g_dev[dv];
+    std::lock_guard<std::mutex> lk(st.mu);
+    if (!st.init && !st.hbuf[0]) continue;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(dv);
+    if (st.d_domain) cudaFree(st.d_domain);
+    if (st.d_counters) cudaFree(st.d_counters);
+    for (int i = 0; i < 4; ++i)
+      if (st.hbuf[i]) cudaFree(st.hbuf[i]);
+    cudaSetDevice(prev);
+    st.d_domain = nullptr;
+    st.d_counters = nullptr;
+    for (int i = 0; i < 4; ++i) { st.hbuf[i] = nullptr; st.hbuf_bytes[i] = 0; }
+    st.init = false;
+    for (bool& a : st.attr_done) a = false;
+  }
+}
+
+}  // extern "C"

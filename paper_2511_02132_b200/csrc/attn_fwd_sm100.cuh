@@ -1,0 +1,450 @@
+// attn_fwd_sm100.cuh -- persistent, warp-specialised FlashAttention-2-style
+// forward kernel for sm_100a (tcgen05 + TMEM + TMA), with the paper's
+// mapping-selectable work scheduler.
+//
+// Math (PAPER.md eq:fa, lines 149-155, and the FA online softmax with its
+// cross-tile "fix-up"): for every query row i of a 128-row
+// block, over key blocks j of 128 keys
+//     S_j  = Q K_j^T                           (tcgen05.mma, fp32 in TMEM)
+//     m'   = max(m, rowmax(S_j))  (kept stale unless it grows by > 8 in log2)
+//     P_j  = exp2(S_j*c - m'*c),  c = scale*log2(e)   (bf16, written to TMEM)
+//     l    = l*exp2((m-m')c) + rowsum(P_j);   O = O*exp2((m-m')c) (fix-up)
+//     O   += P_j V_j                           (tcgen05.mma, A from TMEM)
+// and finally O / l in bf16.
+//
+// CTA layout (384 threads, one CTA per SM, persistent):
+//   warp 0      TMA producer: Q pair, then K_j / V_j into a ring of slots
+//   warp 1      MMA issuer (one thread): S0, S1, PV0, PV1 ... per key block
+//   warp 2      TMEM allocator + work scheduler (atomic pops from the queues
+//               of the active mapping, broadcast through a shared-memory ring)
+//   warp 3      idle
+//   warps 4-7   softmax + fix-up + epilogue of query tile 0 (one row/thread)
+//   warps 8-11  same for query tile 1
+// TMEM (512 columns): S0 [0,128) S1 [128,256) O0 [256,256+D) O1 [256+D,256+2D);
+// P_i (bf16 pairs) aliases the first 64 columns of S_i.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <cstdint>
+
+#include "../../include/attn_numa.h"
+#include "attn_sched.h"
+#include "ptx.cuh"
+
+namespace attn {
+
+constexpr int kBlockM = 128;  // query rows per tile (the paper's BLOCK_M)
+constexpr int kBlockN = 128;  // keys per K/V block
+constexpr int kThreads = 384;
+constexpr int kSchedRing = 2;
+constexpr int kTmemCols = 512;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units; see DESIGN.md "fix-up"
+
+template <int D>
+struct Cfg {
+  static constexpr int kChunks = D / 64;                  // 128-byte swizzle atoms per row
+  static constexpr int kQTileBytes = kBlockM * D * 2;     // one 128-row Q tile
+  static constexpr int kKVBytes = kBlockN * D * 2;        // one K or V block
+  static constexpr int kStages = (D == 128) ? 4 : 8;      // K/V ring slots
+  static constexpr int kOffQ = 0;
+  static constexpr int kOffKV = 2 * kQTileBytes;
+  static constexpr int kOffCtrl = kOffKV + kStages * kKVBytes;
+  static constexpr int kCtrlBytes = 1024;
+  static constexpr int kSmemBytes = kOffCtrl + kCtrlBytes + 1024;  // + alignment slack
+  // TMEM columns: S_t at 128*t, O_t at 256 + D*t
+  static __device__ __forceinline__ uint32_t col_s(int t) { return 128u * t; }
+  static __device__ __forceinline__ uint32_t col_o(int t) { return 256u + (uint32_t)D * t; }
+};
+
+struct KernelParams {
+  int B, Hq, Hkv, N, G, U, nblk;
+  float scale_log2;  // scale * log2(e), >= 0
+  __nv_bfloat16* o;
+  SchedParams sched;
+  int* counters;                 // one int per queue, 32 ints apart
+  const signed char* domain_of_smid;
+  int n_smid;
+  attn_trace_rec_t* trace;
+  long long trace_cap;
+};
+
+struct __align__(16) Ctrl {
+  uint64_t sched_full[kSchedRing];
+  uint64_t sched_empty[kSchedRing];
+  uint64_t q_full, q_empty;
+  uint64_t kv_full[8];
+  uint64_t kv_empty[8];
+  uint64_t s_ready[2];
+  uint64_t p_ready[2];
+  uint64_t o_ready[2];
+  int4 entry[kSchedRing];  // (b, h, u, valid)
+  uint32_t tmem_base;
+};
+
+// Key blocks each tile of unit (u) needs: n0 for block 2u, n1 for block 2u+1.
+template <bool kCausal>
+__device__ __forceinline__ void unit_blocks(int u, int nblk, int& n0, int& n1) {
+  const bool has1 = (2 * u + 1) < nblk;
+  if (kCausal) {  // kBlockN == kBlockM: block qb needs key blocks 0..qb
+    n0 = 2 * u + 1;
+    n1 = has1 ? 2 * u + 2 : 0;
+  } else {
+    n0 = nblk;
+    n1 = has1 ? nblk : 0;
+  }
+}
+
+struct SchedReader {
+  int stage = 0;
+  uint32_t phase = 0;
+  __device__ __forceinline__ int4 next(Ctrl* c, bool arrive) {
+    ptx::mbar_wait(&c->sched_full[stage], phase);
+    const volatile int* ve = reinterpret_cast<const volatile int*>(&c->entry[stage]);
+    const int4 e = make_int4(ve[0], ve[1], ve[2], ve[3]);
+    if (arrive) ptx::mbar_arrive(&c->sched_empty[stage]);
+    if (++stage == kSchedRing) { stage = 0; phase ^= 1; }
+    return e;
+  }
+};
+
+template <int D, bool kCausal>
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                          const __grid_constant__ CUtensorMap tm_v, const KernelParams p) {
+  using C = Cfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* q_smem = smem + C::kOffQ;
+  uint8_t* kv_smem = smem + C::kOffKV;
+  Ctrl* ctrl = reinterpret_cast<Ctrl*>(smem + C::kOffCtrl);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kSchedRing; ++i) {
+      ptx::mbar_init(&ctrl->sched_full[i], 1);
+      ptx::mbar_init(&ctrl->sched_empty[i], 2 + 8);  // TMA + MMA + 8 softmax warps
+    }
+    ptx::mbar_init(&ctrl->q_full, 1);
+    ptx::mbar_init(&ctrl->q_empty, 1);
+    for (int i = 0; i < C::kStages; ++i) {
+      ptx::mbar_init(&ctrl->kv_full[i], 1);
+      ptx::mbar_init(&ctrl->kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&ctrl->s_ready[i], 1);
+      ptx::mbar_init(&ctrl->p_ready[i], 128);
+      ptx::mbar_init(&ctrl->o_ready[i], 1);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&tm_q);
+    ptx::tma_prefetch_desc(&tm_k);
+    ptx::tma_prefetch_desc(&tm_v);
+  }
+  if (warp == 2) {
+    ptx::tmem_alloc(&ctrl->tmem_base, kTmemCols);
+    ptx::tmem_relinquish();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = ctrl->tmem_base;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      SchedReader sr;
+      const uint64_t pol_q = ptx::policy_evict_first();
+      const uint64_t pol_kv = ptx::policy_evict_normal();
+      uint32_t q_phase = 0;
+      int kv_stage = 0;
+      uint32_t kv_phase = 0;
+      while (true) {
+        const int4 e = sr.next(ctrl, true);
+        if (!e.w) break;
+        const int b = e.x, h = e.y, u = e.z;
+        int n0, n1;
+        unit_blocks<kCausal>(u, p.nblk, n0, n1);
+        const int n = n0 > n1 ? n0 : n1;
+        ptx::mbar_wait(&ctrl->q_empty, q_phase ^ 1);
+        q_phase ^= 1;
+        const int ntile = n1 > 0 ? 2 : 1;
+        ptx::mbar_arrive_expect_tx(&ctrl->q_full, ntile * C::kQTileBytes);
+        for (int t = 0; t < ntile; ++t) {
+          const int row = (b * p.Hq + h) * p.N + (2 * u + t) * kBlockM;
+#pragma unroll
+          for (int c = 0; c < C::kChunks; ++c)
+            ptx::tma_load_2d(q_smem + t * C::kQTileBytes + c * kBlockM * 128, &tm_q, &ctrl->q_full, c * 64, row,
+                             pol_q);
+        }
+        const int kvrow = (b * p.Hkv + h / p.G) * p.N;
+        for (int j = 0; j < n; ++j) {
+#pragma unroll
+          for (int which = 0; which < 2; ++which) {
+            ptx::mbar_wait(&ctrl->kv_empty[kv_stage], kv_phase ^ 1);
+            ptx::mbar_arrive_expect_tx(&ctrl->kv_full[kv_stage], C::kKVBytes);
+            uint8_t* dst = kv_smem + kv_stage * C::kKVBytes;
+#pragma unroll
+            for (int c = 0; c < C::kChunks; ++c)
+              ptx::tma_load_2d(dst + c * kBlockN * 128, which == 0 ? (const void*)&tm_k : (const void*)&tm_v,
+                               &ctrl->kv_full[kv_stage], c * 64, kvrow + j * kBlockN, pol_kv);
+            if (++kv_stage == C::kStages) { kv_stage = 0; kv_phase ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // -------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      SchedReader sr;
+      constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(kBlockM, kBlockN, 0, 0);
+      constexpr uint32_t idesc_o = ptx::idesc_bf16_f32(kBlockM, D, 0, 1);
+      const uint32_t q_base = ptx::smem_u32(q_smem);
+      const uint32_t kv_base = ptx::smem_u32(kv_smem);
+      uint32_t q_phase = 0, p_phase[2] = {0, 0};
+      int kv_stage = 0;
+      uint32_t kv_phase = 0;
+
+      auto issue_s = [&](int t, int slot) {
+        const uint32_t qa = q_base + t * C::kQTileBytes;
+        const uint32_t ka = kv_base + slot * C::kKVBytes;
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off_q = (k >> 2) * (kBlockM * 128) + (k & 3) * 32;
+          const uint32_t off_k = (k >> 2) * (kBlockN * 128) + (k & 3) * 32;
+          ptx::mma_ss(tmem + C::col_s(t), ptx::smem_desc_sw128(qa + off_q, 16, 1024),
+                      ptx::smem_desc_sw128(ka + off_k, 16, 1024), idesc_s, k > 0 ? 1u : 0u);
+        }
+      };
+      auto issue_pv = [&](int t, int slot, bool acc) {
+        const uint32_t va = kv_base + slot * C::kKVBytes;
+#pragma unroll
+        for (int k = 0; k < kBlockN / 16; ++k) {
+          ptx::mma_ts(tmem + C::col_o(t), tmem + C::col_s(t) + k * 8,
+                      ptx::smem_desc_sw128(va + k * 16 * 128, kBlockN * 128, 1024), idesc_o,
+                      (acc || k > 0) ? 1u : 0u);
+        }
+      };
+      auto take_slot = [&]() {
+        const int s = kv_stage;
+        ptx::mbar_wait(&ctrl->kv_full[s], kv_phase);
+        if (++kv_stage == C::kStages) { kv_stage = 0; kv_phase ^= 1; }
+        return s;
+      };
+
+      while (true) {
+        const int4 e = sr.next(ctrl, true);
+        if (!e.w) break;
+        int n_t[2];
+        unit_blocks<kCausal>(e.z, p.nblk, n_t[0], n_t[1]);
+        const int n = n_t[0] > n_t[1] ? n_t[0] : n_t[1];
+        ptx::mbar_wait(&ctrl->q_full, q_phase);
+        q_phase ^= 1;
+        int sK = take_slot();
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          if (n_t[t] > 0) {
+            issue_s(t, sK);
+            ptx::mma_commit(&ctrl->s_ready[t]);
+          }
+        }
+        ptx::mma_commit(&ctrl->kv_empty[sK]);
+        if (n == 1) ptx::mma_commit(&ctrl->q_empty);
+        for (int j = 0; j < n; ++j) {
+          const int sV = take_slot();
+          const bool nxt = j + 1 < n;
+          if (nxt) sK = take_slot();
+          ptx::tc_fence_after();
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            if (j < n_t[t]) {
+              ptx::mbar_wait(&ctrl->p_ready[t], p_phase[t]);
+              p_phase[t] ^= 1;
+              ptx::tc_fence_after();
+              issue_pv(t, sV, j > 0);
+              if (j + 1 < n_t[t]) {
+                issue_s(t, sK);
+                ptx::mma_commit(&ctrl->s_ready[t]);
+              } else {
+                ptx::mma_commit(&ctrl->o_ready[t]);
+              }
+            }
+          }
+          ptx::mma_commit(&ctrl->kv_empty[sV]);
+          if (nxt) {
+            ptx::mma_commit(&ctrl->kv_empty[sK]);
+            if (j + 2 == n) ptx::mma_commit(&ctrl->q_empty);
+          }
+        }
+      }
+    }
+  } else if (warp == 2) {
+    // --------------------------------------------------------------- scheduler
+    if (lane == 0) {
+      const int sm = (int)ptx::smid();
+      int dom = (sm < p.n_smid) ? (int)p.domain_of_smid[sm] : 0;
+      if (dom < 0) dom = 0;
+      const int nq = p.sched.n_queues;
+      const int q0 = (nq > 1) ? p.sched.queue_of_domain[dom] : 0;
+      uint32_t exhausted = 0;
+      int stage = 0;
+      uint32_t phase = 0;
+      int seq = 0;
+      while (true) {
+        int b = 0, h = 0, u = 0, qi = -1, stolen = 0;
+        for (int t = 0; t < nq; ++t) {
+          if (t > 0 && !p.sched.steal) break;
+          const int qq = (q0 + t) % nq;
+          if (exhausted & (1u << qq)) continue;
+          const int pos = atomicAdd(&p.counters[qq * 32], 1);
+          if (pos < p.sched.q[qq].len) {
+            decode_unit(p.sched.q[qq], pos, p.Hq, p.U, b, h, u);
+            qi = qq;
+            stolen = t > 0;
+            break;
+          }
+          exhausted |= 1u << qq;
+        }
+        ptx::mbar_wait(&ctrl->sched_empty[stage], phase ^ 1);
+        ctrl->entry[stage] = make_int4(b, h, u, qi >= 0 ? 1 : 0);
+        ptx::mbar_arrive(&ctrl->sched_full[stage]);
+        if (qi < 0) break;
+        if (p.trace) {
+          const long long id = ((long long)b * p.Hq + h) * p.U + u;
+          if (id < p.trace_cap) {
+            attn_trace_rec_t r;
+            r.b = b; r.h = h; r.unit = u; r.smid = sm; r.domain = dom; r.queue = qi;
+            r.stolen = stolen; r.seq = seq; r.t_pop_ns = ptx::globaltimer();
+            p.trace[id] = r;
+          }
+        }
+        ++seq;
+        if (++stage == kSchedRing) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------ softmax / fix-up / epilogue
+    const int t = (warp - 4) >> 2;         // query tile of the unit
+    const int quarter = warp & 3;          // TMEM lane quarter this warp may access
+    const int row = quarter * 32 + lane;   // row within the 128-row tile
+    const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
+    const uint32_t colS = C::col_s(t), colO = C::col_o(t);
+    const float c = p.scale_log2;
+    SchedReader sr;
+    uint32_t s_phase = 0, o_phase = 0;
+    while (true) {
+      const int4 e = sr.next(ctrl, false);
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&ctrl->sched_empty[(sr.stage + kSchedRing - 1) % kSchedRing]);
+      if (!e.w) break;
+      int n_t[2];
+      unit_blocks<kCausal>(e.z, p.nblk, n_t[0], n_t[1]);
+      const int nt = n_t[t];
+      if (nt == 0) continue;
+      const int qb = 2 * e.z + t;
+      float m = -INFINITY, l = 0.f;
+      for (int j = 0; j < nt; ++j) {
+        ptx::mbar_wait(&ctrl->s_ready[t], s_phase);
+        s_phase ^= 1;
+        ptx::tc_fence_after();
+        uint32_t r[128];
+        ptx::tmem_ld64(trow + colS, r);
+        ptx::tmem_ld64(trow + colS + 64, r + 64);
+        const bool diag = kCausal && (j == qb);
+        float mx = -INFINITY;
+        if (diag) {
+#pragma unroll
+          for (int k = 0; k < 128; ++k)
+            if (k <= row) mx = fmaxf(mx, __uint_as_float(r[k]));
+        } else {
+#pragma unroll
+          for (int k = 0; k < 128; ++k) mx = fmaxf(mx, __uint_as_float(r[k]));
+        }
+        float m_use, alpha;
+        bool rescale = false;
+        if (j == 0) {
+          m_use = mx;
+          alpha = 0.f;
+        } else if ((mx - m) * c > kRescaleThreshold) {
+          m_use = mx;
+          alpha = ptx::ex2((m - mx) * c);
+          rescale = true;
+        } else {
+          m_use = m;
+          alpha = 1.f;
+        }
+        const float neg = -m_use * c;
+        float sum = 0.f;
+        if (diag) {
+#pragma unroll
+          for (int k = 0; k < 128; k += 2) {
+            const float p0 = (k <= row) ? ptx::ex2(fmaf(__uint_as_float(r[k]), c, neg)) : 0.f;
+            const float p1 = (k + 1 <= row) ? ptx::ex2(fmaf(__uint_as_float(r[k + 1]), c, neg)) : 0.f;
+            sum += p0 + p1;
+            r[k >> 1] = ptx::pack_bf16(p0, p1);
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < 128; k += 2) {
+            const float p0 = ptx::ex2(fmaf(__uint_as_float(r[k]), c, neg));
+            const float p1 = ptx::ex2(fmaf(__uint_as_float(r[k + 1]), c, neg));
+            sum += p0 + p1;
+            r[k >> 1] = ptx::pack_bf16(p0, p1);
+          }
+        }
+        ptx::tmem_st32(trow + colS, r);
+        ptx::tmem_st32(trow + colS + 32, r + 32);
+        l = (j == 0) ? sum : fmaf(l, alpha, sum);
+        m = m_use;
+        if (__any_sync(0xffffffffu, rescale)) {
+          // fix-up: O *= exp2((m_old - m_new) c) for this row
+#pragma unroll
+          for (int cc = 0; cc < D; cc += 32) {
+            uint32_t o[32];
+            ptx::tmem_ld32(trow + colO + cc, o);
+#pragma unroll
+            for (int k = 0; k < 32; ++k) o[k] = __float_as_uint(__uint_as_float(o[k]) * alpha);
+            ptx::tmem_st32(trow + colO + cc, o);
+          }
+        }
+        ptx::tmem_wait_st();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&ctrl->p_ready[t]);
+      }
+      // ---- epilogue: O / l -> bf16 -> global
+      ptx::mbar_wait(&ctrl->o_ready[t], o_phase);
+      o_phase ^= 1;
+      ptx::tc_fence_after();
+      const float inv_l = 1.f / l;
+      const long long orow = ((long long)(e.x * p.Hq + e.y) * p.N + (long long)qb * kBlockM + row) * D;
+      uint4* dst = reinterpret_cast<uint4*>(p.o + orow);
+#pragma unroll
+      for (int cc = 0; cc < D; cc += 32) {
+        uint32_t o[32];
+        ptx::tmem_ld32(trow + colO + cc, o);
+        uint32_t pk[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+          pk[k] = ptx::pack_bf16(__uint_as_float(o[2 * k]) * inv_l, __uint_as_float(o[2 * k + 1]) * inv_l);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          dst[cc / 8 + k] = make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
+      }
+      ptx::tc_fence_before();
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, kTmemCols);
+  }
+}
+
+}  // namespace attn

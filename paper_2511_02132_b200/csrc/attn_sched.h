@@ -1,0 +1,118 @@
+// attn_sched.h -- work-unit queues for the three mappings (host + device).
+//
+// A work unit is a pair of adjacent 128-row query blocks of one (b, h)
+// (rows [256u, 256u + 256)); the kernel computes both blocks against one K/V
+// stream.  units_per_head U = ceil(N / 256).
+//
+// The paper's mappings become orders over units:
+//   kind 0  block-major range  (Naive Block-first):
+//           pos -> b = pos / (U*Hq), u = (pos % (U*Hq)) / Hq, h = pos % Hq
+//   kind 1  head-major range   (Naive Head-first; also SHF queues cut
+//           over the global (b, ACC) list or at unit granularity):
+//           hm = start + pos -> b = hm / (Hq*U), h = (hm / U) % Hq, u = hm % U
+//   kind 2  per-batch head range (Swizzled Head-first, Fig. 7 with
+//           batch outermost): queue d holds, for every b, heads
+//           [h_lo, h_lo + h_cnt) (whole ACCs) in head-major order.
+// Block-first and head-first use ONE queue popped by every SM of every die;
+// swizzled head-first uses one queue per die (reading R8).
+#pragma once
+#include <cstdint>
+
+#ifndef ATTN_HD
+#ifdef __CUDACC__
+#define ATTN_HD __host__ __device__ __forceinline__
+#else
+#define ATTN_HD inline
+#endif
+#endif
+
+namespace attn {
+
+constexpr int kMaxQueues = 8;
+
+struct QueueDesc {
+  int kind;   // 0 block-major range, 1 head-major range, 2 per-batch head range
+  int start;  // first position (kinds 0, 1)
+  int len;    // number of units in the queue
+  int h_lo;   // kind 2: first query head
+  int h_cnt;  // kind 2: number of query heads per batch item
+};
+
+struct SchedParams {
+  int n_queues;
+  int steal;                           // pop other queues when the own one is empty
+  int queue_of_domain[kMaxQueues];     // die -> queue popped first
+  QueueDesc q[kMaxQueues];
+};
+
+ATTN_HD void decode_unit(const QueueDesc& qd, int pos, int Hq, int U, int& b, int& h, int& u) {
+  if (qd.kind == 0) {
+    const int p = qd.start + pos;
+    b = p / (U * Hq);
+    const int r = p % (U * Hq);
+    u = r / Hq;
+    h = r % Hq;
+  } else if (qd.kind == 1) {
+    const int hm = qd.start + pos;
+    b = hm / (Hq * U);
+    h = (hm / U) % Hq;
+    u = hm % U;
+  } else {
+    const int per_b = qd.h_cnt * U;
+    b = pos / per_b;
+    const int r = pos % per_b;
+    h = qd.h_lo + r / U;
+    u = r % U;
+  }
+}
+
+// Proportional contiguous cut of [0, total) by die sizes (rounded to nearest).
+inline int prop_cut(long long total, const int* sizes, int n, int d) {
+  long long S = 0, acc = 0;
+  for (int e = 0; e < n; ++e) S += sizes[e];
+  for (int e = 0; e < d; ++e) acc += sizes[e];
+  if (d >= n) return (int)total;
+  return (int)((total * acc + S / 2) / S);
+}
+
+// Build the queues of `mapping` (0 BF, 1 HF, 2 SHF) for n_domains dies.
+// Returns false on bad arguments.
+inline bool build_sched(int mapping, int B, int Hq, int Hkv, int U, int n_domains, const int* sms_per_domain,
+                        SchedParams& sp) {
+  sp = SchedParams{};
+  if (B <= 0 || Hq <= 0 || Hkv <= 0 || U <= 0 || Hq % Hkv != 0) return false;
+  if (n_domains < 1 || n_domains > kMaxQueues) return false;
+  const int G = Hq / Hkv;
+  const int total = B * Hq * U;
+  if (mapping == 0 || mapping == 1 || n_domains == 1) {
+    sp.n_queues = 1;
+    sp.steal = 0;
+    sp.q[0] = QueueDesc{mapping == 0 ? 0 : 1, 0, total, 0, Hq};
+    return mapping >= 0 && mapping <= 2;
+  }
+  if (mapping != 2) return false;
+  const int D = n_domains;
+  sp.n_queues = D;
+  sp.steal = 1;
+  for (int d = 0; d < D; ++d) sp.queue_of_domain[d] = d;
+  if (Hkv >= D) {
+    for (int d = 0; d < D; ++d) {
+      const int a0 = prop_cut(Hkv, sms_per_domain, D, d), a1 = prop_cut(Hkv, sms_per_domain, D, d + 1);
+      sp.q[d] = QueueDesc{2, 0, B * (a1 - a0) * G * U, a0 * G, (a1 - a0) * G};
+    }
+  } else if ((long long)B * Hkv >= D) {
+    const int A = B * Hkv;
+    for (int d = 0; d < D; ++d) {
+      const int a0 = prop_cut(A, sms_per_domain, D, d), a1 = prop_cut(A, sms_per_domain, D, d + 1);
+      sp.q[d] = QueueDesc{1, a0 * G * U, (a1 - a0) * G * U, 0, Hq};
+    }
+  } else {
+    for (int d = 0; d < D; ++d) {
+      const int t0 = prop_cut(total, sms_per_domain, D, d), t1 = prop_cut(total, sms_per_domain, D, d + 1);
+      sp.q[d] = QueueDesc{1, t0, t1 - t0, 0, Hq};
+    }
+  }
+  return true;
+}
+
+}  // namespace attn

@@ -1,0 +1,152 @@
+"""GPU parity: the sm_100a kernel (through the C-ABI) vs the fp64 CPU oracle.
+
+Tolerance (north star, BASELINE.json): max |O_gpu - O_oracle| <= 2e-2 and
+mean |O_gpu - O_oracle| <= 2e-3, element by element, on bf16 inputs drawn
+i.i.d. N(0,1) (paper_2511_02132_b200/synth.py).  Every mapping must give the
+same output bit for bit.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import attn as oa
+from paper_2511_02132_b200 import attn_fwd, synth
+
+pytestmark = pytest.mark.gpu
+
+MAX_TOL = 2e-2
+MEAN_TOL = 2e-3
+MAPS = ("block_first", "head_first", "swizzled_head_first")
+
+
+def _check(out: torch.Tensor, ref: np.ndarray, what: str):
+    got = out.float().cpu().numpy().astype(np.float64)
+    assert np.all(np.isfinite(got)), f"{what}: non-finite output"
+    err = np.abs(got - ref)
+    assert err.max() <= MAX_TOL, f"{what}: max abs err {err.max():.3e}"
+    assert err.mean() <= MEAN_TOL, f"{what}: mean abs err {err.mean():.3e}"
+    return err
+
+
+def _run(q, k, v, causal, mapping, scale=None):
+    o = torch.full_like(q, float("nan"))
+    attn_fwd(q, k, v, o, causal=causal, mapping=mapping, scale=scale)
+    torch.cuda.synchronize()
+    return o
+
+
+# Full-tensor parity at sizes the oracle finishes in seconds: several tiles,
+# odd block counts (a unit with one tile), GQA, both head dims.
+SMALL = [
+    # B, Hq, Hkv, N, d, causal
+    (1, 2, 2, 128, 64, False),    # C1 shape (one 128-row block, one half-empty unit)
+    (1, 2, 2, 128, 64, True),
+    (1, 2, 2, 256, 128, False),
+    (1, 2, 2, 256, 128, True),
+    (2, 4, 2, 384, 64, True),     # GQA, 3 blocks per head (ragged unit)
+    (1, 3, 3, 640, 128, False),   # 5 blocks per head, odd head count
+    (2, 8, 2, 512, 128, True),
+    (1, 4, 1, 1024, 64, True),    # MQA
+]
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,N,d,causal", SMALL)
+def test_small_full_parity_all_mappings(B, Hq, Hkv, N, d, causal):
+    q, k, v = synth.make_qkv(B, Hq, Hkv, N, d, base=1, device="cuda")
+    ref = oa.attention(q.cpu(), k.cpu(), v.cpu(), causal=causal, scale=1.0 / math.sqrt(d))
+    outs = []
+    for m in MAPS:
+        o = _run(q, k, v, causal, m)
+        _check(o, ref, f"{m} {B}x{Hq}/{Hkv}x{N}x{d} causal={causal}")
+        outs.append(o)
+    for o in outs[1:]:
+        assert torch.equal(o.view(torch.int16), outs[0].view(torch.int16)), "mappings differ bitwise"
+
+
+def _sample_rows(B, Hq, N, n, seed):
+    rng = np.random.default_rng(seed)
+    rows = []
+    edges = [0, 1, 127, 128, 129, 255, 256, N - 129, N - 128, N - 2, N - 1]
+    for i in edges:
+        rows.append((int(rng.integers(B)), int(rng.integers(Hq)), i))
+    while len(rows) < n:
+        rows.append((int(rng.integers(B)), int(rng.integers(Hq)), int(rng.integers(N))))
+    return np.array(rows, dtype=np.int64)
+
+
+# BASELINE.json configs 2-4 at full size (config 5 in test_gpu_large), sampled rows.
+FULL = [
+    ("C2", 1, 32, 32, 8192, 128, False),
+    ("C3", 1, 128, 128, 32768, 128, True),
+    ("C4", 2, 64, 8, 16384, 128, True),
+]
+
+
+@pytest.mark.parametrize("name,B,Hq,Hkv,N,d,causal", FULL)
+def test_full_size_sampled_rows(name, B, Hq, Hkv, N, d, causal):
+    q, k, v = synth.make_qkv(B, Hq, Hkv, N, d, base=2, device="cuda")
+    o = _run(q, k, v, causal, "swizzled_head_first")
+    rows = _sample_rows(B, Hq, N, 96 if N >= 16384 else 160, 7)
+    ref = oa.attention_rows(q.cpu(), k.cpu(), v.cpu(), rows, causal=causal, scale=1.0 / math.sqrt(d))
+    got = o[rows[:, 0], rows[:, 1], rows[:, 2]]
+    _check(got, ref, name)
+    assert not torch.isnan(o.float()).any(), "unwritten output elements"
+    o2 = _run(q, k, v, causal, "block_first")
+    assert torch.equal(o.view(torch.int16), o2.view(torch.int16))
+
+
+def test_causal_row0_is_v0_bitexact():
+    q, k, v = synth.make_qkv(1, 4, 4, 512, 128, base=3, device="cuda")
+    o = _run(q, k, v, True, "swizzled_head_first")
+    assert torch.equal(o[:, :, 0].view(torch.int16), v[:, :, 0].view(torch.int16))
+
+
+def test_causal_ignores_future_keys_bitexact():
+    q, k, v = synth.make_qkv(1, 2, 2, 512, 64, base=4, device="cuda")
+    o = _run(q, k, v, True, "head_first")
+    k2, v2 = k.clone(), v.clone()
+    k2[:, :, 300:] = 3.0
+    v2[:, :, 300:] = -7.0
+    o2 = _run(q, k2, v2, True, "head_first")
+    assert torch.equal(o[:, :, :300].view(torch.int16), o2[:, :, :300].view(torch.int16))
+
+
+def test_constant_v():
+    q, k, _ = synth.make_qkv(1, 2, 2, 384, 128, base=5, device="cuda")
+    v = torch.full_like(k, 0.0)
+    v += (torch.arange(128, device="cuda", dtype=torch.float32) / 64.0 - 1.0).to(torch.bfloat16)
+    o = _run(q, k, v, False, "swizzled_head_first")
+    err = (o.float() - v.float()).abs().max().item()
+    assert err <= 1e-2
+
+
+def test_scale_zero_uniform():
+    q, k, v = synth.make_qkv(1, 2, 2, 256, 64, base=6, device="cuda")
+    o = _run(q, k, v, False, "head_first", scale=0.0)
+    ref = v.double().mean(dim=2, keepdim=True).expand_as(o)
+    assert (o.double() - ref).abs().max().item() <= 2e-2
+
+
+def test_gqa_equals_mha_repeated_bitexact():
+    q, k, v = synth.make_qkv(2, 8, 2, 256, 128, base=7, device="cuda")
+    o = _run(q, k, v, True, "swizzled_head_first")
+    o2 = _run(q, k.repeat_interleave(4, 1).contiguous(), v.repeat_interleave(4, 1).contiguous(), True,
+              "swizzled_head_first")
+    assert torch.equal(o.view(torch.int16), o2.view(torch.int16))
+
+
+def test_head_shards_concatenate_bitexact():
+    """Heads computed alone (what a rank of a head-sharded run does) equal the full run."""
+    B, Hq, Hkv, N, d = 1, 8, 8, 512, 128
+    q, k, v = synth.make_qkv(B, Hq, Hkv, N, d, base=8, device="cuda")
+    full = _run(q, k, v, True, "swizzled_head_first")
+    G = 4
+    for r in range(G):
+        sl = slice(r * Hq // G, (r + 1) * Hq // G)
+        qs, ks, vs = synth.make_qkv(B, Hq // G, Hkv // G, N, d, base=8, q_head_offset=sl.start,
+                                    kv_head_offset=sl.start, device="cuda")
+        assert torch.equal(qs, q[:, sl])
+        part = _run(qs, ks, vs, True, "swizzled_head_first")
+        assert torch.equal(part.view(torch.int16), full[:, sl].view(torch.int16))
