@@ -9,7 +9,7 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libattnnuma.so")
+LIB_PATH = os.environ.get("ATTN_NUMA_LIB") or os.path.join(_PKG, "lib", "libattnnuma.so")
 
 ATTN_MAX_DOMAINS = 8
 ATTN_MAX_SMID = 512

@@ -40,22 +40,26 @@ def needs_build() -> bool:
     return any(os.path.getmtime(s) > t for s in _sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str = LIB) -> str:
+    """Compile api.cu (which includes every kernel) into `out`.  `defines` are
+    extra -D flags for experiment variants (the default build uses none)."""
+    if not force and not defines and out == LIB and not needs_build():
         return LIB
-    os.makedirs(LIB_DIR, exist_ok=True)
-    cmd = [NVCC, *NVCC_FLAGS]
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    cmd = [NVCC, *NVCC_FLAGS] + [f"-D{d}" for d in defines]
     if verbose:
         cmd += ["-Xptxas", "-v"]
-    cmd += [os.path.join(CSRC, "api.cu"), "-o", LIB + ".tmp"]
+    cmd += [os.path.join(CSRC, "api.cu"), "-o", out + ".tmp"]
     subprocess.check_call(cmd)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("-D", dest="defines", action="append", default=[])
+    ap.add_argument("--out", default=LIB)
     a = ap.parse_args()
-    print(build(force=a.force, verbose=a.verbose))
+    print(build(force=a.force, verbose=a.verbose, defines=a.defines, out=a.out))

@@ -14,7 +14,7 @@
 //
 // CTA layout (384 threads, one CTA per SM, persistent):
 //   warp 0      TMA producer: Q pair, then K_j / V_j into a ring of slots
-//   warp 1      MMA issuer (one thread): S0, S1, PV0, PV1 ... per key block
+//   warp 1      MMA issuer (one elected lane): S0, S1, PV0, PV1 ... per key block
 //   warp 2      TMEM allocator + work scheduler (atomic pops from the queues
 //               of the active mapping, broadcast through a shared-memory ring)
 //   warp 3      idle
@@ -40,6 +40,17 @@ constexpr int kThreads = 384;
 constexpr int kSchedRing = 2;
 constexpr int kTmemCols = 512;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units; see DESIGN.md "fix-up"
+#ifndef ATTN_EMU_PERIOD
+#define ATTN_EMU_PERIOD 0
+#endif
+#ifndef ATTN_SETMAXNREG
+#define ATTN_SETMAXNREG 1
+#endif
+constexpr int kEmuPeriod = ATTN_EMU_PERIOD;  // every kEmuPeriod-th exp2 pair runs on the FMA pipe (0: none)
+// Register split (setmaxnreg): 128 threads of warps 0-3 give registers to the
+// 256 softmax threads: 128*80 + 256*208 = 63488 <= 65536.
+constexpr int kOtherRegs = 80;
+constexpr int kSoftmaxRegs = 208;
 
 template <int D>
 struct Cfg {
@@ -125,7 +136,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < kSchedRing; ++i) {
       ptx::mbar_init(&ctrl->sched_full[i], 1);
-      ptx::mbar_init(&ctrl->sched_empty[i], 2 + 8);  // TMA + MMA + 8 softmax warps
+      ptx::mbar_init(&ctrl->sched_empty[i], 2 + 8);  // TMA + MMA + 8 softmax warps (one arrive each)
     }
     ptx::mbar_init(&ctrl->q_full, 1);
     ptx::mbar_init(&ctrl->q_empty, 1);
@@ -135,7 +146,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&ctrl->s_ready[i], 1);
-      ptx::mbar_init(&ctrl->p_ready[i], 128);
+      ptx::mbar_init(&ctrl->p_ready[i], 4);  // one arrive per softmax warp
       ptx::mbar_init(&ctrl->o_ready[i], 1);
     }
     ptx::fence_barrier_init();
@@ -152,10 +163,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
-  const uint32_t tmem = ctrl->tmem_base;
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
+    if (ATTN_SETMAXNREG) ptx::setmaxnreg_dec<kOtherRegs>();
     if (lane == 0) {
       SchedReader sr;
       const uint64_t pol_q = ptx::policy_evict_first();
@@ -199,92 +210,123 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // -------------------------------------------------------------- MMA issuer
-    if (lane == 0) {
-      SchedReader sr;
-      constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(kBlockM, kBlockN, 0, 0);
-      constexpr uint32_t idesc_o = ptx::idesc_bf16_f32(kBlockM, D, 0, 1);
-      const uint32_t q_base = ptx::smem_u32(q_smem);
-      const uint32_t kv_base = ptx::smem_u32(kv_smem);
-      uint32_t q_phase = 0, p_phase[2] = {0, 0};
-      int kv_stage = 0;
-      uint32_t kv_phase = 0;
+    // The whole warp runs the control flow (warp-uniform values stay in
+    // uniform registers); one elected lane issues tcgen05.mma / commit.
+    if (ATTN_SETMAXNREG) ptx::setmaxnreg_dec<kOtherRegs>();
+    const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(&ctrl->tmem_base);
+    SchedReader sr;
+    constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(kBlockM, kBlockN, 0, 0);
+    constexpr uint32_t idesc_o = ptx::idesc_bf16_f32(kBlockM, D, 0, 1);
+    // descriptors at k = 0; advancing K by 16 elements adds 32 B (2 in the
+    // >>4 address field) inside a 128-byte swizzle atom, and one atom
+    // (rows * 128 B) every 4 steps.
+    const uint64_t dq0 = ptx::smem_desc_sw128(ptx::smem_u32(q_smem), 16, 1024);
+    const uint64_t dkv0 = ptx::smem_desc_sw128(ptx::smem_u32(kv_smem), 16, 1024);
+    const uint64_t dv0 = ptx::smem_desc_sw128(ptx::smem_u32(kv_smem), kBlockN * 128, 1024);
+    uint32_t q_phase = 0, p_phase0 = 0, p_phase1 = 0;
+    int kv_stage = 0;
+    uint32_t kv_phase = 0;
 
-      auto issue_s = [&](int t, int slot) {
-        const uint32_t qa = q_base + t * C::kQTileBytes;
-        const uint32_t ka = kv_base + slot * C::kKVBytes;
+    auto issue_s = [&](int t, int slot) {
+      const uint64_t dq = dq0 + (uint64_t)((t * C::kQTileBytes) >> 4);
+      const uint64_t dk = dkv0 + (uint64_t)((slot * C::kKVBytes) >> 4);
+      const uint32_t d_tmem = tmem + C::col_s(t);
 #pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint32_t off_q = (k >> 2) * (kBlockM * 128) + (k & 3) * 32;
-          const uint32_t off_k = (k >> 2) * (kBlockN * 128) + (k & 3) * 32;
-          ptx::mma_ss(tmem + C::col_s(t), ptx::smem_desc_sw128(qa + off_q, 16, 1024),
-                      ptx::smem_desc_sw128(ka + off_k, 16, 1024), idesc_s, k > 0 ? 1u : 0u);
-        }
-      };
-      auto issue_pv = [&](int t, int slot, bool acc) {
-        const uint32_t va = kv_base + slot * C::kKVBytes;
+      for (int k = 0; k < D / 16; ++k) {
+        const uint32_t oq = ((k >> 2) * (kBlockM * 128) + (k & 3) * 32) >> 4;
+        const uint32_t ok = ((k >> 2) * (kBlockN * 128) + (k & 3) * 32) >> 4;
+        ptx::mma_ss(d_tmem, dq + oq, dk + ok, idesc_s, k > 0 ? 1u : 0u);
+      }
+    };
+    auto issue_pv = [&](int t, int slot, bool acc) {
+      const uint64_t dv = dv0 + (uint64_t)((slot * C::kKVBytes) >> 4);
+      const uint32_t d_tmem = tmem + C::col_o(t);
+      const uint32_t a_tmem = tmem + C::col_s(t);
 #pragma unroll
-        for (int k = 0; k < kBlockN / 16; ++k) {
-          ptx::mma_ts(tmem + C::col_o(t), tmem + C::col_s(t) + k * 8,
-                      ptx::smem_desc_sw128(va + k * 16 * 128, kBlockN * 128, 1024), idesc_o,
-                      (acc || k > 0) ? 1u : 0u);
-        }
-      };
-      auto take_slot = [&]() {
-        const int s = kv_stage;
-        ptx::mbar_wait(&ctrl->kv_full[s], kv_phase);
-        if (++kv_stage == C::kStages) { kv_stage = 0; kv_phase ^= 1; }
-        return s;
-      };
+      for (int k = 0; k < kBlockN / 16; ++k)
+        ptx::mma_ts(d_tmem, a_tmem + k * 8, dv + (uint64_t)((k * 16 * 128) >> 4), idesc_o,
+                    (acc || k > 0) ? 1u : 0u);
+    };
+    auto take_slot = [&]() {
+      const int s = kv_stage;
+      ptx::mbar_wait(&ctrl->kv_full[s], kv_phase);
+      if (++kv_stage == C::kStages) { kv_stage = 0; kv_phase ^= 1; }
+      return s;
+    };
 
-      while (true) {
-        const int4 e = sr.next(ctrl, true);
-        if (!e.w) break;
-        int n_t[2];
-        unit_blocks<kCausal>(e.z, p.nblk, n_t[0], n_t[1]);
-        const int n = n_t[0] > n_t[1] ? n_t[0] : n_t[1];
-        ptx::mbar_wait(&ctrl->q_full, q_phase);
-        q_phase ^= 1;
-        int sK = take_slot();
-        ptx::tc_fence_after();
-#pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          if (n_t[t] > 0) {
-            issue_s(t, sK);
-            ptx::mma_commit(&ctrl->s_ready[t]);
-          }
+    while (true) {
+      const int4 e = sr.next(ctrl, false);
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&ctrl->sched_empty[(sr.stage + kSchedRing - 1) % kSchedRing]);
+      if (!e.w) break;
+      int n0, n1;
+      unit_blocks<kCausal>(e.z, p.nblk, n0, n1);
+      const int n = n0 > n1 ? n0 : n1;
+      ptx::mbar_wait(&ctrl->q_full, q_phase);
+      q_phase ^= 1;
+      int sK = take_slot();
+      ptx::tc_fence_after();
+      if (ptx::elect_one_sync()) {
+        if (n0 > 0) {
+          issue_s(0, sK);
+          ptx::mma_commit(&ctrl->s_ready[0]);
+        }
+        if (n1 > 0) {
+          issue_s(1, sK);
+          ptx::mma_commit(&ctrl->s_ready[1]);
         }
         ptx::mma_commit(&ctrl->kv_empty[sK]);
         if (n == 1) ptx::mma_commit(&ctrl->q_empty);
-        for (int j = 0; j < n; ++j) {
-          const int sV = take_slot();
-          const bool nxt = j + 1 < n;
-          if (nxt) sK = take_slot();
+      }
+      __syncwarp();
+      for (int j = 0; j < n; ++j) {
+        const int sV = take_slot();
+        const bool nxt = j + 1 < n;
+        if (nxt) sK = take_slot();
+        ptx::tc_fence_after();
+        if (j < n0) {
+          ptx::mbar_wait(&ctrl->p_ready[0], p_phase0);
+          p_phase0 ^= 1;
           ptx::tc_fence_after();
-#pragma unroll
-          for (int t = 0; t < 2; ++t) {
-            if (j < n_t[t]) {
-              ptx::mbar_wait(&ctrl->p_ready[t], p_phase[t]);
-              p_phase[t] ^= 1;
-              ptx::tc_fence_after();
-              issue_pv(t, sV, j > 0);
-              if (j + 1 < n_t[t]) {
-                issue_s(t, sK);
-                ptx::mma_commit(&ctrl->s_ready[t]);
-              } else {
-                ptx::mma_commit(&ctrl->o_ready[t]);
-              }
+          if (ptx::elect_one_sync()) {
+            issue_pv(0, sV, j > 0);
+            if (j + 1 < n0) {
+              issue_s(0, sK);
+              ptx::mma_commit(&ctrl->s_ready[0]);
+            } else {
+              ptx::mma_commit(&ctrl->o_ready[0]);
             }
           }
+          __syncwarp();
+        }
+        if (j < n1) {
+          ptx::mbar_wait(&ctrl->p_ready[1], p_phase1);
+          p_phase1 ^= 1;
+          ptx::tc_fence_after();
+          if (ptx::elect_one_sync()) {
+            issue_pv(1, sV, j > 0);
+            if (j + 1 < n1) {
+              issue_s(1, sK);
+              ptx::mma_commit(&ctrl->s_ready[1]);
+            } else {
+              ptx::mma_commit(&ctrl->o_ready[1]);
+            }
+          }
+          __syncwarp();
+        }
+        if (ptx::elect_one_sync()) {
           ptx::mma_commit(&ctrl->kv_empty[sV]);
           if (nxt) {
             ptx::mma_commit(&ctrl->kv_empty[sK]);
             if (j + 2 == n) ptx::mma_commit(&ctrl->q_empty);
           }
         }
+        __syncwarp();
       }
     }
   } else if (warp == 2) {
     // --------------------------------------------------------------- scheduler
+    if (ATTN_SETMAXNREG) ptx::setmaxnreg_dec<kOtherRegs>();
     if (lane == 0) {
       const int sm = (int)ptx::smid();
       int dom = (sm < p.n_smid) ? (int)p.domain_of_smid[sm] : 0;
@@ -329,6 +371,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // ------------------------------------------------ softmax / fix-up / epilogue
+    if (ATTN_SETMAXNREG) ptx::setmaxnreg_inc<kSoftmaxRegs>();
+    const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(&ctrl->tmem_base);
     const int t = (warp - 4) >> 2;         // query tile of the unit
     const int quarter = warp & 3;          // TMEM lane quarter this warp may access
     const int row = quarter * 32 + lane;   // row within the 128-row tile
@@ -344,7 +388,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (!e.w) break;
       int n_t[2];
       unit_blocks<kCausal>(e.z, p.nblk, n_t[0], n_t[1]);
-      const int nt = n_t[t];
+      const int nt = (t == 0) ? n_t[0] : n_t[1];
       if (nt == 0) continue;
       const int qb = 2 * e.z + t;
       float m = -INFINITY, l = 0.f;
@@ -352,19 +396,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::mbar_wait(&ctrl->s_ready[t], s_phase);
         s_phase ^= 1;
         ptx::tc_fence_after();
+#ifdef ATTN_DEBUG_SKIP_SOFTMAX
+        if (lane == 0) ptx::mbar_arrive(&ctrl->p_ready[t]);
+        l = 1.f;
+        continue;
+#endif
         uint32_t r[128];
-        ptx::tmem_ld64(trow + colS, r);
-        ptx::tmem_ld64(trow + colS + 64, r + 64);
+        ptx::tmem_ld128(trow + colS, r);
         const bool diag = kCausal && (j == qb);
-        float mx = -INFINITY;
-        if (diag) {
+        if (diag) {  // causal mask on the diagonal block: key k > row -> -inf
 #pragma unroll
           for (int k = 0; k < 128; ++k)
-            if (k <= row) mx = fmaxf(mx, __uint_as_float(r[k]));
-        } else {
-#pragma unroll
-          for (int k = 0; k < 128; ++k) mx = fmaxf(mx, __uint_as_float(r[k]));
+            if (k > row) r[k] = 0xff800000u;
         }
+        // row max with four independent FMNMX3 chains
+        float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+        for (int k = 0; k < 128; k += 8) {
+#pragma unroll
+          for (int g = 0; g < 4; ++g)
+            mq[g] = fmaxf(mq[g], fmaxf(__uint_as_float(r[k + 2 * g]), __uint_as_float(r[k + 2 * g + 1])));
+        }
+        const float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
         float m_use, alpha;
         bool rescale = false;
         if (j == 0) {
@@ -379,26 +432,30 @@ __global__ void __launch_bounds__(kThreads, 1)
           alpha = 1.f;
         }
         const float neg = -m_use * c;
-        float sum = 0.f;
-        if (diag) {
+        // P = exp2(S c - m c): MUFU.EX2 for most pairs, an FMA-pipe polynomial
+        // for every kEmuPeriod-th pair (balances the MUFU and FMA pipes).
+        float sq[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-          for (int k = 0; k < 128; k += 2) {
-            const float p0 = (k <= row) ? ptx::ex2(fmaf(__uint_as_float(r[k]), c, neg)) : 0.f;
-            const float p1 = (k + 1 <= row) ? ptx::ex2(fmaf(__uint_as_float(r[k + 1]), c, neg)) : 0.f;
-            sum += p0 + p1;
-            r[k >> 1] = ptx::pack_bf16(p0, p1);
+        for (int k = 0; k < 128; k += 2) {
+          const float x0 = fmaf(__uint_as_float(r[k]), c, neg);
+          const float x1 = fmaf(__uint_as_float(r[k + 1]), c, neg);
+          float p0, p1;
+          if (kEmuPeriod > 0 && ((k >> 1) % (kEmuPeriod > 0 ? kEmuPeriod : 1)) == kEmuPeriod - 1) {
+            p0 = ptx::ex2_poly(x0);
+            p1 = ptx::ex2_poly(x1);
+          } else {
+            p0 = ptx::ex2(x0);
+            p1 = ptx::ex2(x1);
           }
-        } else {
-#pragma unroll
-          for (int k = 0; k < 128; k += 2) {
-            const float p0 = ptx::ex2(fmaf(__uint_as_float(r[k]), c, neg));
-            const float p1 = ptx::ex2(fmaf(__uint_as_float(r[k + 1]), c, neg));
-            sum += p0 + p1;
-            r[k >> 1] = ptx::pack_bf16(p0, p1);
+          if (diag) {
+            p0 = (k <= row) ? p0 : 0.f;
+            p1 = (k + 1 <= row) ? p1 : 0.f;
           }
+          sq[(k >> 1) & 3] += p0 + p1;
+          r[k >> 1] = ptx::pack_bf16(p0, p1);
         }
-        ptx::tmem_st32(trow + colS, r);
-        ptx::tmem_st32(trow + colS + 32, r + 32);
+        ptx::tmem_st64(trow + colS, r);
+        const float sum = (sq[0] + sq[1]) + (sq[2] + sq[3]);
         l = (j == 0) ? sum : fmaf(l, alpha, sum);
         m = m_use;
         if (__any_sync(0xffffffffu, rescale)) {
@@ -414,7 +471,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
-        ptx::mbar_arrive(&ctrl->p_ready[t]);
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&ctrl->p_ready[t]);
       }
       // ---- epilogue: O / l -> bf16 -> global
       ptx::mbar_wait(&ctrl->o_ready[t], o_phase);
@@ -437,13 +495,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       ptx::tc_fence_before();
     }
+  } else {
+    if (ATTN_SETMAXNREG) ptx::setmaxnreg_dec<kOtherRegs>();  // warp 3: idle
   }
 
   ptx::tc_fence_before();
   __syncthreads();
   if (warp == 2) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem, kTmemCols);
+    ptx::tmem_dealloc(*reinterpret_cast<volatile uint32_t*>(&ctrl->tmem_base), kTmemCols);
   }
 }
 

@@ -51,7 +51,7 @@ __global__ void topo_latency_kernel(const uint32_t* probe, int* claimed, uint32_
   // warm: touch every line once (brings it into L2)
   for (int i = 0; i < kProbeLines; ++i) {
     uint32_t x;
-    asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(x) : "l"(base + (size_t)i * kProbeStrideBytes) : "memory");
+    asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(x) : "l"(base + (size_t)i * kProbeStrideBytes) : "memory");
     sink += x;
   }
   for (int i = 0; i < kProbeLines; ++i) {
@@ -61,7 +61,7 @@ __global__ void topo_latency_kernel(const uint32_t* probe, int* claimed, uint32_
       const long long t0 = clock64();
 #pragma unroll
       for (int c = 0; c < kChain; ++c)
-        asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(off) : "l"(base + off) : "memory");
+        asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(off) : "l"(base + off) : "memory");
       sink += off;
       const long long t1 = clock64();
       const uint32_t dt = (uint32_t)((t1 - t0) / kChain);
