@@ -41,11 +41,12 @@ constexpr int kSchedRing = 2;
 constexpr int kTmemCols = 512;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units; see DESIGN.md "fix-up"
 #ifndef ATTN_EMU_PERIOD
-#define ATTN_EMU_PERIOD 0
+#define ATTN_EMU_PERIOD 8
 #endif
 #ifndef ATTN_SETMAXNREG
 #define ATTN_SETMAXNREG 1
 #endif
+
 constexpr int kEmuPeriod = ATTN_EMU_PERIOD;  // every kEmuPeriod-th exp2 pair runs on the FMA pipe (0: none)
 // Register split (setmaxnreg): 128 threads of warps 0-3 give registers to the
 // 256 softmax threads: 128*80 + 256*208 = 63488 <= 65536.
@@ -386,9 +387,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&ctrl->sched_empty[(sr.stage + kSchedRing - 1) % kSchedRing]);
       if (!e.w) break;
-      int n_t[2];
-      unit_blocks<kCausal>(e.z, p.nblk, n_t[0], n_t[1]);
-      const int nt = (t == 0) ? n_t[0] : n_t[1];
+      int n0, n1;
+      unit_blocks<kCausal>(e.z, p.nblk, n0, n1);
+      const int nt = (t == 0) ? n0 : n1;
       if (nt == 0) continue;
       const int qb = 2 * e.z + t;
       float m = -INFINITY, l = 0.f;
@@ -397,6 +398,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         s_phase ^= 1;
         ptx::tc_fence_after();
 #ifdef ATTN_DEBUG_SKIP_SOFTMAX
+        __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&ctrl->p_ready[t]);
         l = 1.f;
         continue;
@@ -414,8 +416,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int k = 0; k < 128; k += 8) {
 #pragma unroll
-          for (int g = 0; g < 4; ++g)
-            mq[g] = fmaxf(mq[g], fmaxf(__uint_as_float(r[k + 2 * g]), __uint_as_float(r[k + 2 * g + 1])));
+          for (int g4 = 0; g4 < 4; ++g4)
+            mq[g4] = fmaxf(mq[g4], fmaxf(__uint_as_float(r[k + 2 * g4]), __uint_as_float(r[k + 2 * g4 + 1])));
         }
         const float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
         float m_use, alpha;
@@ -432,30 +434,32 @@ __global__ void __launch_bounds__(kThreads, 1)
           alpha = 1.f;
         }
         const float neg = -m_use * c;
-        // P = exp2(S c - m c): MUFU.EX2 for most pairs, an FMA-pipe polynomial
-        // for every kEmuPeriod-th pair (balances the MUFU and FMA pipes).
-        float sq[4] = {0.f, 0.f, 0.f, 0.f};
+        // P = exp2(S c - m c) on (even, odd) pairs with packed f32x2 math:
+        // MUFU.EX2 for most pairs, the FMA-pipe polynomial for every
+        // kEmuPeriod-th pair (moves work off the MUFU unit).
+        float2 sq[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                        make_float2(0.f, 0.f)};
 #pragma unroll
         for (int k = 0; k < 128; k += 2) {
-          const float x0 = fmaf(__uint_as_float(r[k]), c, neg);
-          const float x1 = fmaf(__uint_as_float(r[k + 1]), c, neg);
-          float p0, p1;
+          const float2 x = ptx::ffma2(make_float2(__uint_as_float(r[k]), __uint_as_float(r[k + 1])), c, neg);
+          float2 pr;
           if (kEmuPeriod > 0 && ((k >> 1) % (kEmuPeriod > 0 ? kEmuPeriod : 1)) == kEmuPeriod - 1) {
-            p0 = ptx::ex2_poly(x0);
-            p1 = ptx::ex2_poly(x1);
+            pr = ptx::ex2_poly2(x);
           } else {
-            p0 = ptx::ex2(x0);
-            p1 = ptx::ex2(x1);
+            pr.x = ptx::ex2(x.x);
+            pr.y = ptx::ex2(x.y);
           }
           if (diag) {
-            p0 = (k <= row) ? p0 : 0.f;
-            p1 = (k + 1 <= row) ? p1 : 0.f;
+            pr.x = (k <= row) ? pr.x : 0.f;
+            pr.y = (k + 1 <= row) ? pr.y : 0.f;
           }
-          sq[(k >> 1) & 3] += p0 + p1;
-          r[k >> 1] = ptx::pack_bf16(p0, p1);
+          sq[(k >> 1) & 3] = ptx::fadd2(sq[(k >> 1) & 3], pr);
+          r[k >> 1] = ptx::pack_bf16(pr.x, pr.y);
         }
         ptx::tmem_st64(trow + colS, r);
-        const float sum = (sq[0] + sq[1]) + (sq[2] + sq[3]);
+        const float2 s01 = ptx::fadd2(sq[0], sq[1]), s23 = ptx::fadd2(sq[2], sq[3]);
+        const float2 s4 = ptx::fadd2(s01, s23);
+        const float sum = s4.x + s4.y;
         l = (j == 0) ? sum : fmaf(l, alpha, sum);
         m = m_use;
         if (__any_sync(0xffffffffu, rescale)) {
