@@ -25,7 +25,7 @@ using namespace attn;
 
 constexpr int kMaxDevices = 16;
 constexpr int kCounterSlots = 64;
-constexpr int kCounterInts = kMaxQueues * 32;  // one 128-byte line per queue
+constexpr int kCounterInts = (kMaxQueues + 1) * 32;  // one 128-byte line per queue + done count
 
 thread_local std::string g_err;
 thread_local cudaStream_t g_stream = nullptr;
@@ -110,43 +110,73 @@ int probe_once(int nsmid, const uint32_t* d_probe, std::vector<uint32_t>& lat, i
   return ATTN_OK;
 }
 
-// Classify SMs into dies from a latency matrix.  Returns false if inconclusive.
+// Classify SMs into dies from a latency matrix (returns false if inconclusive).
+// Every SM's vector of per-line latencies is centred on its own mean; SMs of
+// one die see the same lines as near/far, so their vectors are close.  Two
+// centroids are seeded with SM s0 and the SM farthest from it, then refined
+// by 2-means (Lloyd).  The split is accepted if the centroids differ by at
+// least 8 cycles on average over the lines (near ~235 vs far ~265 cycles).
 bool classify(const std::vector<uint32_t>& lat, const std::vector<int>& present, signed char* dom, float& near_c,
               float& far_c) {
-  std::vector<double> all;
-  for (int s : present)
-    for (int l = 0; l < kProbeLines; ++l) all.push_back((double)lat[(size_t)s * kProbeLines + l]);
-  if (all.size() < 2) return false;
-  std::sort(all.begin(), all.end());
-  double c0 = all[all.size() / 10], c1 = all[all.size() * 9 / 10];
-  for (int it = 0; it < 50; ++it) {
-    const double thr = 0.5 * (c0 + c1);
-    double s0 = 0, s1 = 0;
-    size_t n0 = 0, n1 = 0;
-    for (double x : all) {
-      if (x < thr) { s0 += x; ++n0; } else { s1 += x; ++n1; }
-    }
-    if (n0 == 0 || n1 == 0) return false;
-    c0 = s0 / n0;
-    c1 = s1 / n1;
+  const int S = (int)present.size(), L = kProbeLines;
+  if (S < 2) return false;
+  std::vector<double> z((size_t)S * L);
+  for (int i = 0; i < S; ++i) {
+    double mean = 0;
+    for (int l = 0; l < L; ++l) mean += lat[(size_t)present[i] * L + l];
+    mean /= L;
+    for (int l = 0; l < L; ++l) z[(size_t)i * L + l] = lat[(size_t)present[i] * L + l] - mean;
   }
-  near_c = (float)c0;
-  far_c = (float)c1;
-  if (c1 - c0 < 8.0) return false;
-  const double thr = 0.5 * (c0 + c1);
-  const int s_ref = present[0];
-  int count[2] = {0, 0};
-  for (int s : present) {
-    int agree = 0;
-    for (int l = 0; l < kProbeLines; ++l) {
-      const bool a = lat[(size_t)s * kProbeLines + l] < thr;
-      const bool b = lat[(size_t)s_ref * kProbeLines + l] < thr;
-      agree += (a == b);
-    }
-    dom[s] = (2 * agree > kProbeLines) ? 0 : 1;
-    ++count[(int)dom[s]];
+  auto dist2 = [&](const double* a, const double* b) {
+    double d = 0;
+    for (int l = 0; l < L; ++l) d += (a[l] - b[l]) * (a[l] - b[l]);
+    return d;
+  };
+  int far_i = 0;
+  double best = -1;
+  for (int i = 0; i < S; ++i) {
+    const double d = dist2(&z[0], &z[(size_t)i * L]);
+    if (d > best) { best = d; far_i = i; }
   }
-  return count[0] > 0 && count[1] > 0;
+  std::vector<double> c0(z.begin(), z.begin() + L), c1(z.begin() + (size_t)far_i * L, z.begin() + (size_t)far_i * L + L);
+  std::vector<int> lab(S, 0);
+  for (int it = 0; it < 30; ++it) {
+    for (int i = 0; i < S; ++i) lab[i] = dist2(&z[(size_t)i * L], c1.data()) < dist2(&z[(size_t)i * L], c0.data());
+    lab[0] = 0;  // s0 defines die 0
+    std::vector<double> n0(L, 0), n1(L, 0);
+    int k0 = 0, k1 = 0;
+    for (int i = 0; i < S; ++i) {
+      auto& c = lab[i] ? n1 : n0;
+      for (int l = 0; l < L; ++l) c[l] += z[(size_t)i * L + l];
+      (lab[i] ? k1 : k0)++;
+    }
+    if (k0 == 0 || k1 == 0) return false;
+    for (int l = 0; l < L; ++l) { c0[l] = n0[l] / k0; c1[l] = n1[l] / k1; }
+  }
+  double sep = 0;
+  for (int l = 0; l < L; ++l) sep += std::fabs(c0[l] - c1[l]);
+  sep /= L;
+  // near/far latency: per line, the lower / higher of the two clusters' raw means
+  std::vector<double> nearv, farv;
+  for (int l = 0; l < L; ++l) {
+    double m0 = 0, m1 = 0;
+    int k0 = 0, k1 = 0;
+    for (int i = 0; i < S; ++i) {
+      const double x = lat[(size_t)present[i] * L + l];
+      if (lab[i]) { m1 += x; ++k1; } else { m0 += x; ++k0; }
+    }
+    m0 /= k0;
+    m1 /= k1;
+    nearv.push_back(std::min(m0, m1));
+    farv.push_back(std::max(m0, m1));
+  }
+  std::sort(nearv.begin(), nearv.end());
+  std::sort(farv.begin(), farv.end());
+  near_c = (float)nearv[L / 2];
+  far_c = (float)farv[L / 2];
+  if (sep < 8.0) return false;
+  for (int i = 0; i < S; ++i) dom[present[i]] = (signed char)lab[i];
+  return true;
 }
 
 int run_probe(int dev, DevState& st) {
@@ -389,7 +419,6 @@ int fwd_impl(const void* q, const void* k, const void* v, void* o, int B, int Hq
   if ((rc = make_tmap(&tk, k, (long long)B * Hkv * N, d)) != ATTN_OK) return rc;
   if ((rc = make_tmap(&tv, v, (long long)B * Hkv * N, d)) != ATTN_OK) return rc;
 
-  ATTN_CUDA(cudaMemsetAsync(kp.counters, 0, sizeof(int) * kCounterInts, stream));
   const int total = B * Hq * U;
   const int grid = std::min(st.num_sms, total);
   if (d == 128 && causal) rc = launch_t<128, true>(st, 0, tq, tk, tv, kp, grid, stream);

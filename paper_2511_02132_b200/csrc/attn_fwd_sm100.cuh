@@ -39,6 +39,7 @@ constexpr int kBlockN = 128;  // keys per K/V block
 constexpr int kThreads = 384;
 constexpr int kSchedRing = 2;
 constexpr int kTmemCols = 512;
+constexpr int kDoneCounter = kMaxQueues * 32;  // counters[] index of the CTA-done count
 constexpr float kRescaleThreshold = 8.0f;  // log2 units; see DESIGN.md "fix-up"
 #ifndef ATTN_EMU_PERIOD
 #define ATTN_EMU_PERIOD 8
@@ -74,7 +75,7 @@ struct KernelParams {
   float scale_log2;  // scale * log2(e), >= 0
   __nv_bfloat16* o;
   SchedParams sched;
-  int* counters;                 // one int per queue, 32 ints apart
+  int* counters;                 // one int per queue, 32 ints apart, then the done count
   const signed char* domain_of_smid;
   int n_smid;
   attn_trace_rec_t* trace;
@@ -368,6 +369,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         ++seq;
         if (++stage == kSchedRing) { stage = 0; phase ^= 1; }
+      }
+      // Self-resetting counters: the last CTA to finish popping zeroes the
+      // queue counters for the next launch on this slot (no host memset).
+      __threadfence();
+      if (atomicAdd(&p.counters[kDoneCounter], 1) == (int)gridDim.x - 1) {
+        for (int q = 0; q < nq; ++q) atomicExch(&p.counters[q * 32], 0);
+        atomicExch(&p.counters[kDoneCounter], 0);
+        __threadfence();
       }
     }
   } else if (warp >= 4) {

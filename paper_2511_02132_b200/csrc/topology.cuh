@@ -23,7 +23,7 @@ namespace attn {
 
 constexpr int kProbeLines = 128;
 constexpr int kProbeStrideBytes = 4096;
-constexpr int kProbeRounds = 4;
+constexpr int kProbeRounds = 8;
 
 __global__ void topo_census_kernel(int* smid_seen, int* nsmid_out) {
   if (threadIdx.x == 0) {

@@ -1,0 +1,93 @@
+"""Head sharding across the GPUs of one node.
+
+PAPER.md:167: "Each grid cell operates independently with no data reuse
+between heads or batch items."  Rank r of G therefore owns KV heads
+[r*Hkv/G, (r+1)*Hkv/G) and their query heads [r*Hq/G, (r+1)*Hq/G) for every
+batch item, and runs attn_fwd on that shard with NO communication.  Inside
+each GPU the paper's mapping logic is unchanged (swizzled head-first splits
+the rank's ACCs across its two dies).
+
+The only collectives are optional: an all-gather of O when the caller asks
+for replicated output, and the max-over-ranks of timings.  torch.distributed
+(NCCL on GPUs, gloo in the CPU tests) is plumbing only.
+"""
+from __future__ import annotations
+
+import os
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+import torch.distributed as dist
+
+
+@dataclass(frozen=True)
+class HeadShard:
+    rank: int
+    world: int
+    q_lo: int
+    q_hi: int
+    kv_lo: int
+    kv_hi: int
+
+    @property
+    def hq(self) -> int:
+        return self.q_hi - self.q_lo
+
+    @property
+    def hkv(self) -> int:
+        return self.kv_hi - self.kv_lo
+
+
+def shard_heads(Hq: int, Hkv: int, rank: int, world: int) -> HeadShard:
+    """Contiguous KV-head ranges (whole GQA groups) per rank; needs Hkv % world == 0."""
+    if world <= 0 or not (0 <= rank < world):
+        raise ValueError("bad rank/world")
+    if Hq % Hkv != 0:
+        raise ValueError("Hq % Hkv != 0")
+    if Hkv % world != 0:
+        raise ValueError(f"Hkv={Hkv} is not divisible by world={world}: heads cannot be sharded evenly")
+    G = Hq // Hkv
+    per = Hkv // world
+    kv_lo, kv_hi = rank * per, (rank + 1) * per
+    return HeadShard(rank, world, kv_lo * G, kv_hi * G, kv_lo, kv_hi)
+
+
+def env_rank_world():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), \
+        int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def init(backend: Optional[str] = None) -> tuple:
+    """Initialise the default process group from torchrun's env (127.0.0.1 rendezvous)."""
+    rank, world, local = env_rank_world()
+    if world > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if backend is None:
+            backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    return rank, world, local
+
+
+def all_gather_heads(o_local: torch.Tensor, world: int, group=None) -> torch.Tensor:
+    """Replicated O from per-rank head shards [B, Hq/G, N, d] -> [B, Hq, N, d]."""
+    B, hq, N, d = o_local.shape
+    if world == 1:
+        return o_local
+    buf = torch.empty((world, B, hq, N, d), dtype=o_local.dtype, device=o_local.device)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(buf, o_local.contiguous(), group=group)  # NVLink / NVSwitch
+    else:
+        dist.all_gather(list(buf.unbind(0)), o_local.contiguous(), group=group)
+    return buf.permute(1, 0, 2, 3, 4).reshape(B, world * hq, N, d)
+
+
+def max_over_ranks(x: float, device=None) -> float:
+    """Max of a scalar over all ranks (timing aggregation)."""
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(x)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())

@@ -1,0 +1,95 @@
+"""The C-ABI boundary without a GPU: the library loads, exports every symbol
+include/attn_numa.h declares, validates arguments synchronously (status codes
+before any CUDA call), and its host-side queue builder reproduces the
+mapping reference in oracle/mapping.py exactly (integer work: bit-exact)."""
+import ctypes
+import os
+import random
+import re
+
+import pytest
+
+from oracle import mapping as om
+from paper_2511_02132_b200 import _lib, api
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "attn_numa.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2511_02132_b200 import build
+
+    build.build()
+    return _lib.load()
+
+
+def test_header_exports_match(lib):
+    declared = set(re.findall(r"ATTN_API\s+[\w\s\*]+?\b(attn_\w+)\s*\(", open(HEADER).read()))
+    assert declared == set(_lib.EXPORTS), declared ^ set(_lib.EXPORTS)
+    for name in declared:
+        assert hasattr(lib, name), f"{name} not exported"
+    out = os.popen(f"nm -D --defined-only {_lib.LIB_PATH}").read()
+    exported = set(re.findall(r"\bT (attn_\w+)", out))
+    assert declared <= exported
+
+
+def test_status_strings_and_version(lib):
+    assert lib.attn_status_string(0) == b"ATTN_OK"
+    assert lib.attn_status_string(1) == b"ATTN_ERR_INVALID_VALUE"
+    assert lib.attn_status_string(2) == b"ATTN_ERR_UNSUPPORTED"
+    assert b"sm_100a" in lib.attn_version()
+
+
+def _fwd(lib, q=1 << 20, k=2 << 20, v=3 << 20, o=4 << 20, B=1, Hq=2, Hkv=2, N=128, d=64, causal=0, scale=0.125,
+         mapping=2):
+    return lib.attn_fwd(q, k, v, o, B, Hq, Hkv, N, d, causal, scale, mapping)
+
+
+@pytest.mark.parametrize("kw,status", [
+    (dict(q=0), 1), (dict(o=0), 1), (dict(B=0), 1), (dict(N=-1), 1), (dict(Hq=6, Hkv=4), 1),
+    (dict(mapping=3), 1), (dict(mapping=-1), 1), (dict(scale=float("nan")), 1), (dict(scale=float("inf")), 1),
+    (dict(d=96), 2), (dict(N=200), 2), (dict(scale=-0.5), 2), (dict(q=(1 << 20) + 8), 2),
+    (dict(o=(1 << 20) + 64), 1),   # o overlaps q
+])
+def test_invalid_arguments_rejected_before_launch(lib, kw, status):
+    assert _fwd(lib, **kw) == status
+    assert len(lib.attn_last_error()) > 0
+
+
+def test_non_device_pointers_rejected(lib):
+    # plausible arguments but host addresses: never reaches a launch
+    buf = (ctypes.c_uint16 * (4 * 2 * 128 * 64))()
+    base = ctypes.addressof(buf)
+    n = 2 * 128 * 64 * 2
+    rc = lib.attn_fwd(base, base + n, base + 2 * n, base + 3 * n, 1, 2, 2, 128, 64, 0, 0.125, 2)
+    assert rc != 0
+
+
+def test_topology_override_validates(lib):
+    assert lib.attn_set_topology_override(-1, None, 0, 0) != 0
+
+
+@pytest.mark.parametrize("mapping", om.MAPPINGS)
+def test_schedule_order_matches_oracle(lib, mapping):
+    rng = random.Random(7)
+    for _ in range(60):
+        Hkv = rng.choice([1, 2, 3, 4, 8, 16])
+        Hq = Hkv * rng.choice([1, 2, 4])
+        B = rng.randint(1, 3)
+        N = 128 * rng.randint(1, 12)
+        sizes = [rng.randint(60, 80) for _ in range(rng.randint(1, 3))]
+        U = (N + 255) // 256
+        got = api.attn_schedule_order(B, Hq, Hkv, N, mapping, sizes)
+        want = om.build_queues(mapping, B, Hq, Hkv, U, sizes)
+        assert got == want, (mapping, B, Hq, Hkv, N, sizes)
+
+
+def test_schedule_order_baseline_configs(lib):
+    """The BASELINE configs on B200's measured 74/74 split: SHF co-locates every ACC."""
+    for (B, Hq, Hkv, N) in ((1, 32, 32, 8192), (1, 128, 128, 32768), (2, 64, 8, 16384)):
+        q = api.attn_schedule_order(B, Hq, Hkv, N, "swizzled_head_first", [74, 74])
+        assert len(q) == 2 and abs(len(q[0]) - len(q[1])) <= (N // 256) * (Hq // Hkv)
+        doms = om.acc_domains(q, Hq, Hkv)
+        assert all(len(s) == 1 for s in doms.values())
+        assert om.is_bijection(q, B, Hq, N // 256)
