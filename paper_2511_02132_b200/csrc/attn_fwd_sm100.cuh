@@ -36,7 +36,14 @@ namespace attn {
 
 constexpr int kBlockM = 128;  // query rows per tile (the paper's BLOCK_M)
 constexpr int kBlockN = 128;  // keys per K/V block
-constexpr int kThreads = 384;
+#ifndef ATTN_SPLIT
+#define ATTN_SPLIT 1
+#endif
+// softmax warps per (tile, TMEM lane quarter): each handles kBlockN / kSplit
+// columns of its 32 rows, so two warps share each SMSP's MUFU per tile.
+constexpr int kSplit = ATTN_SPLIT;
+constexpr int kSoftmaxWarps = 8 * kSplit;
+constexpr int kThreads = 128 + 32 * kSoftmaxWarps;
 constexpr int kSchedRing = 2;
 constexpr int kTmemCols = 512;
 constexpr int kDoneCounter = kMaxQueues * 32;  // counters[] index of the CTA-done count
@@ -49,10 +56,16 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units; see DESIGN.md "fix-up"
 #endif
 
 constexpr int kEmuPeriod = ATTN_EMU_PERIOD;  // every kEmuPeriod-th exp2 pair runs on the FMA pipe (0: none)
-// Register split (setmaxnreg): 128 threads of warps 0-3 give registers to the
-// 256 softmax threads: 128*80 + 256*208 = 63488 <= 65536.
-constexpr int kOtherRegs = 80;
-constexpr int kSoftmaxRegs = 208;
+// Register split (setmaxnreg).  The CTA's register pool is what the launch
+// allocated: kThreads * kInitRegs (ptxas caps a thread at 65536 / kThreads,
+// rounded down to a multiple of 8).  Warps 0-3 release registers that the
+// softmax warps then claim; .inc blocks forever if the pool is short, so the
+// budget is checked at compile time.
+constexpr int kInitRegs = ((65536 / kThreads) / 8) * 8;
+constexpr int kOtherRegs = (kSplit == 1) ? 80 : 64;
+constexpr int kSoftmaxRegs = (kSplit == 1) ? 208 : 104;
+static_assert(128 * (kInitRegs - kOtherRegs) >= 32 * kSoftmaxWarps * (kSoftmaxRegs - kInitRegs),
+              "setmaxnreg budget exceeds the CTA register pool");
 
 template <int D>
 struct Cfg {
@@ -63,7 +76,7 @@ struct Cfg {
   static constexpr int kOffQ = 0;
   static constexpr int kOffKV = 2 * kQTileBytes;
   static constexpr int kOffCtrl = kOffKV + kStages * kKVBytes;
-  static constexpr int kCtrlBytes = 1024;
+  static constexpr int kCtrlBytes = 8192;
   static constexpr int kSmemBytes = kOffCtrl + kCtrlBytes + 1024;  // + alignment slack
   // TMEM columns: S_t at 128*t, O_t at 256 + D*t
   static __device__ __forceinline__ uint32_t col_s(int t) { return 128u * t; }
@@ -89,10 +102,12 @@ struct __align__(16) Ctrl {
   uint64_t kv_full[8];
   uint64_t kv_empty[8];
   uint64_t s_ready[2];
-  uint64_t p_ready[2];
+  uint64_t p_ready[2][2];   // [tile][half of P]  softmax -> MMA
   uint64_t o_ready[2];
   int4 entry[kSchedRing];  // (b, h, u, valid)
   uint32_t tmem_base;
+  float red[2][4][2][2][32];   // [tile][quarter][half][parity][lane] partial row max
+  float lsum[2][4][2][32];     // [tile][quarter][half][lane] partial row sum (epilogue)
 };
 
 // Key blocks each tile of unit (u) needs: n0 for block 2u, n1 for block 2u+1.
@@ -138,7 +153,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < kSchedRing; ++i) {
       ptx::mbar_init(&ctrl->sched_full[i], 1);
-      ptx::mbar_init(&ctrl->sched_empty[i], 2 + 8);  // TMA + MMA + 8 softmax warps (one arrive each)
+      ptx::mbar_init(&ctrl->sched_empty[i], 2 + kSoftmaxWarps);  // TMA + MMA + softmax warps (one arrive each)
     }
     ptx::mbar_init(&ctrl->q_full, 1);
     ptx::mbar_init(&ctrl->q_empty, 1);
@@ -148,7 +163,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&ctrl->s_ready[i], 1);
-      ptx::mbar_init(&ctrl->p_ready[i], 4);  // one arrive per softmax warp
+      ptx::mbar_init(&ctrl->p_ready[i][0], 4 * kSplit);  // one arrive per softmax warp of the tile
+      ptx::mbar_init(&ctrl->p_ready[i][1], 4 * kSplit);
       ptx::mbar_init(&ctrl->o_ready[i], 1);
     }
     ptx::fence_barrier_init();
@@ -240,12 +256,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::mma_ss(d_tmem, dq + oq, dk + ok, idesc_s, k > 0 ? 1u : 0u);
       }
     };
-    auto issue_pv = [&](int t, int slot, bool acc) {
+    // O_t += P_t V: K = 128 keys in 8 steps of 16; steps [4h, 4h+4) read the
+    // half h of P, which the softmax publishes separately (p_ready[t][h]).
+    auto issue_pv_half = [&](int t, int slot, bool acc, int h) {
       const uint64_t dv = dv0 + (uint64_t)((slot * C::kKVBytes) >> 4);
       const uint32_t d_tmem = tmem + C::col_o(t);
       const uint32_t a_tmem = tmem + C::col_s(t);
 #pragma unroll
-      for (int k = 0; k < kBlockN / 16; ++k)
+      for (int k = 4 * h; k < 4 * h + 4; ++k)
         ptx::mma_ts(d_tmem, a_tmem + k * 8, dv + (uint64_t)((k * 16 * 128) >> 4), idesc_o,
                     (acc || k > 0) ? 1u : 0u);
     };
@@ -286,35 +304,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool nxt = j + 1 < n;
         if (nxt) sK = take_slot();
         ptx::tc_fence_after();
-        if (j < n0) {
-          ptx::mbar_wait(&ctrl->p_ready[0], p_phase0);
-          p_phase0 ^= 1;
-          ptx::tc_fence_after();
-          if (ptx::elect_one_sync()) {
-            issue_pv(0, sV, j > 0);
-            if (j + 1 < n0) {
-              issue_s(0, sK);
-              ptx::mma_commit(&ctrl->s_ready[0]);
-            } else {
-              ptx::mma_commit(&ctrl->o_ready[0]);
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const int nt = (t == 0) ? n0 : n1;
+          if (j < nt) {
+            const uint32_t ph = (t == 0) ? p_phase0 : p_phase1;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              ptx::mbar_wait(&ctrl->p_ready[t][h], ph);
+              ptx::tc_fence_after();
+              if (ptx::elect_one_sync()) issue_pv_half(t, sV, j > 0, h);
+              __syncwarp();
             }
-          }
-          __syncwarp();
-        }
-        if (j < n1) {
-          ptx::mbar_wait(&ctrl->p_ready[1], p_phase1);
-          p_phase1 ^= 1;
-          ptx::tc_fence_after();
-          if (ptx::elect_one_sync()) {
-            issue_pv(1, sV, j > 0);
-            if (j + 1 < n1) {
-              issue_s(1, sK);
-              ptx::mma_commit(&ctrl->s_ready[1]);
-            } else {
-              ptx::mma_commit(&ctrl->o_ready[1]);
+            if (t == 0) p_phase0 ^= 1; else p_phase1 ^= 1;
+            if (ptx::elect_one_sync()) {
+              if (j + 1 < nt) {
+                issue_s(t, sK);
+                ptx::mma_commit(&ctrl->s_ready[t]);
+              } else {
+                ptx::mma_commit(&ctrl->o_ready[t]);
+              }
             }
+            __syncwarp();
           }
-          __syncwarp();
         }
         if (ptx::elect_one_sync()) {
           ptx::mma_commit(&ctrl->kv_empty[sV]);
@@ -383,14 +395,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------ softmax / fix-up / epilogue
     if (ATTN_SETMAXNREG) ptx::setmaxnreg_inc<kSoftmaxRegs>();
     const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(&ctrl->tmem_base);
-    const int t = (warp - 4) >> 2;         // query tile of the unit
-    const int quarter = warp & 3;          // TMEM lane quarter this warp may access
-    const int row = quarter * 32 + lane;   // row within the 128-row tile
+    constexpr int kCols = kBlockN / kSplit;  // S columns per thread
+    constexpr int kOCols = D / kSplit;       // O columns per thread (fix-up, epilogue)
+    const int sw = warp - 4;
+    const int t = sw / (4 * kSplit);         // query tile of the unit
+    const int hf = (sw >> 2) % kSplit;       // which column slice of the row
+    const int quarter = warp & 3;            // TMEM lane quarter this warp may access
+    const int row = quarter * 32 + lane;     // row within the 128-row tile
+    const int cbase = hf * kCols;            // first key column of this thread's slice
     const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
-    const uint32_t colS = C::col_s(t), colO = C::col_o(t);
+    const uint32_t colS = C::col_s(t) + cbase;
+    const uint32_t colP = C::col_s(t) + cbase / 2;
+    const uint32_t colO = C::col_o(t) + hf * kOCols;
+    [[maybe_unused]] const uint32_t bar_id = 1 + t * 4 + quarter;  // named barrier of the row group's warps
     const float c = p.scale_log2;
     SchedReader sr;
-    uint32_t s_phase = 0, o_phase = 0;
+    uint32_t s_phase = 0, o_phase = 0, gblk = 0;
     while (true) {
       const int4 e = sr.next(ctrl, false);
       __syncwarp();
@@ -401,34 +421,41 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int nt = (t == 0) ? n0 : n1;
       if (nt == 0) continue;
       const int qb = 2 * e.z + t;
+      const int lim = row - cbase;  // diagonal block: local key k visible iff k <= lim
       float m = -INFINITY, l = 0.f;
-      for (int j = 0; j < nt; ++j) {
+      for (int j = 0; j < nt; ++j, ++gblk) {
         ptx::mbar_wait(&ctrl->s_ready[t], s_phase);
         s_phase ^= 1;
         ptx::tc_fence_after();
 #ifdef ATTN_DEBUG_SKIP_SOFTMAX
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&ctrl->p_ready[t]);
+        if (lane == 0) { ptx::mbar_arrive(&ctrl->p_ready[t][0]); ptx::mbar_arrive(&ctrl->p_ready[t][1]); }
         l = 1.f;
         continue;
 #endif
-        uint32_t r[128];
-        ptx::tmem_ld128(trow + colS, r);
+        uint32_t r[kCols];
+        if constexpr (kCols == 128) ptx::tmem_ld128(trow + colS, r);
+        else ptx::tmem_ld64(trow + colS, r);
         const bool diag = kCausal && (j == qb);
-        if (diag) {  // causal mask on the diagonal block: key k > row -> -inf
+        if (diag) {  // causal mask on the diagonal block: key > row -> -inf
 #pragma unroll
-          for (int k = 0; k < 128; ++k)
-            if (k > row) r[k] = 0xff800000u;
+          for (int k = 0; k < kCols; ++k)
+            if (k > lim) r[k] = 0xff800000u;
         }
-        // row max with four independent FMNMX3 chains
+        // row max: four independent FMNMX3 chains, then across the kSplit warps
         float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-        for (int k = 0; k < 128; k += 8) {
+        for (int k = 0; k < kCols; k += 8) {
 #pragma unroll
           for (int g4 = 0; g4 < 4; ++g4)
             mq[g4] = fmaxf(mq[g4], fmaxf(__uint_as_float(r[k + 2 * g4]), __uint_as_float(r[k + 2 * g4 + 1])));
         }
-        const float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
+        float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
+        if constexpr (kSplit == 2) {
+          ctrl->red[t][quarter][hf][gblk & 1][lane] = mx;
+          ptx::named_bar_sync(bar_id, 64);
+          mx = fmaxf(mx, ctrl->red[t][quarter][hf ^ 1][gblk & 1][lane]);
+        }
         float m_use, alpha;
         bool rescale = false;
         if (j == 0) {
@@ -442,39 +469,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           m_use = m;
           alpha = 1.f;
         }
-        const float neg = -m_use * c;
-        // P = exp2(S c - m c) on (even, odd) pairs with packed f32x2 math:
-        // MUFU.EX2 for most pairs, the FMA-pipe polynomial for every
-        // kEmuPeriod-th pair (moves work off the MUFU unit).
-        float2 sq[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
-                        make_float2(0.f, 0.f)};
-#pragma unroll
-        for (int k = 0; k < 128; k += 2) {
-          const float2 x = ptx::ffma2(make_float2(__uint_as_float(r[k]), __uint_as_float(r[k + 1])), c, neg);
-          float2 pr;
-          if (kEmuPeriod > 0 && ((k >> 1) % (kEmuPeriod > 0 ? kEmuPeriod : 1)) == kEmuPeriod - 1) {
-            pr = ptx::ex2_poly2(x);
-          } else {
-            pr.x = ptx::ex2(x.x);
-            pr.y = ptx::ex2(x.y);
-          }
-          if (diag) {
-            pr.x = (k <= row) ? pr.x : 0.f;
-            pr.y = (k + 1 <= row) ? pr.y : 0.f;
-          }
-          sq[(k >> 1) & 3] = ptx::fadd2(sq[(k >> 1) & 3], pr);
-          r[k >> 1] = ptx::pack_bf16(pr.x, pr.y);
-        }
-        ptx::tmem_st64(trow + colS, r);
-        const float2 s01 = ptx::fadd2(sq[0], sq[1]), s23 = ptx::fadd2(sq[2], sq[3]);
-        const float2 s4 = ptx::fadd2(s01, s23);
-        const float sum = s4.x + s4.y;
-        l = (j == 0) ? sum : fmaf(l, alpha, sum);
-        m = m_use;
         if (__any_sync(0xffffffffu, rescale)) {
-          // fix-up: O *= exp2((m_old - m_new) c) for this row
+          // fix-up: O *= exp2((m_old - m_new) c) for this row;
+          // PV_t(j-1) is complete (it precedes S_t(j) in the MMA stream).
 #pragma unroll
-          for (int cc = 0; cc < D; cc += 32) {
+          for (int cc = 0; cc < kOCols; cc += 32) {
             uint32_t o[32];
             ptx::tmem_ld32(trow + colO + cc, o);
 #pragma unroll
@@ -482,20 +481,59 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::tmem_st32(trow + colO + cc, o);
           }
         }
-        ptx::tmem_wait_st();
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&ctrl->p_ready[t]);
+        const float neg = -m_use * c;
+        // P = exp2(S c - m c) on (even, odd) pairs with packed f32x2 math:
+        // MUFU.EX2 for most pairs, the FMA-pipe polynomial for every
+        // kEmuPeriod-th pair.  P is published in two halves so the tensor
+        // core starts O += P V on the first half while the second is computed.
+        float2 sq[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                        make_float2(0.f, 0.f)};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+#pragma unroll
+          for (int k = h * kCols / 2; k < (h + 1) * kCols / 2; k += 2) {
+            const float2 x = ptx::ffma2(make_float2(__uint_as_float(r[k]), __uint_as_float(r[k + 1])), c, neg);
+            float2 pr;
+            if (kEmuPeriod > 0 && ((k >> 1) % (kEmuPeriod > 0 ? kEmuPeriod : 1)) == kEmuPeriod - 1) {
+              pr = ptx::ex2_poly2(x);
+            } else {
+              pr.x = ptx::ex2(x.x);
+              pr.y = ptx::ex2(x.y);
+            }
+            if (diag) {
+              pr.x = (k <= lim) ? pr.x : 0.f;
+              pr.y = (k + 1 <= lim) ? pr.y : 0.f;
+            }
+            sq[(k >> 1) & 3] = ptx::fadd2(sq[(k >> 1) & 3], pr);
+            r[k >> 1] = ptx::pack_bf16(pr.x, pr.y);
+          }
+          if constexpr (kCols == 128) ptx::tmem_st32(trow + colP + h * 32, r + h * 32);
+          else ptx::tmem_st16(trow + colP + h * 16, r + h * 16);
+          ptx::tmem_wait_st();
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&ctrl->p_ready[t][h]);
+        }
+        const float2 s01 = ptx::fadd2(sq[0], sq[1]), s23 = ptx::fadd2(sq[2], sq[3]);
+        const float2 s4 = ptx::fadd2(s01, s23);
+        const float sum = s4.x + s4.y;
+        l = (j == 0) ? sum : fmaf(l, alpha, sum);
+        m = m_use;
       }
       // ---- epilogue: O / l -> bf16 -> global
+      if constexpr (kSplit == 2) {
+        ctrl->lsum[t][quarter][hf][lane] = l;
+        ptx::named_bar_sync(bar_id, 64);
+        l += ctrl->lsum[t][quarter][hf ^ 1][lane];
+      }
       ptx::mbar_wait(&ctrl->o_ready[t], o_phase);
       o_phase ^= 1;
       ptx::tc_fence_after();
       const float inv_l = 1.f / l;
       const long long orow = ((long long)(e.x * p.Hq + e.y) * p.N + (long long)qb * kBlockM + row) * D;
-      uint4* dst = reinterpret_cast<uint4*>(p.o + orow);
+      uint4* dst = reinterpret_cast<uint4*>(p.o + orow + hf * kOCols);
 #pragma unroll
-      for (int cc = 0; cc < D; cc += 32) {
+      for (int cc = 0; cc < kOCols; cc += 32) {
         uint32_t o[32];
         ptx::tmem_ld32(trow + colO + cc, o);
         uint32_t pk[16];
