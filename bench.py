@@ -35,7 +35,7 @@ WORKLOADS = {
     "C5": (1, 128, 128, 131072, 128, True, "strong"),
 }
 METRIC = "attention fwd TFLOP/s (% of bf16 peak) and L2 hit rate by mapping, 1/2/4/8 B200"
-MAPS = ("block_first", "head_first", "swizzled_head_first")
+MAPS = ("block_first", "head_first", "swizzled_head_first", "swizzled_block_first")
 
 
 def flops_fwd(B, Hq, N, d, causal) -> float:

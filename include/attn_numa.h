@@ -17,6 +17,10 @@
  *        every unit of one Attention Compute Cluster (a head, or a GQA
  *        group) is processed on SMs of one die, each die
  *        serving its ACCs one at a time.
+ *   ATTN_MAP_SWIZZLED_BLOCK_FIRST Swizzled Block-first   (PAPER.md:236-243,
+ *        SPEC.md:172): block-first order with KV group g pinned to die
+ *        g mod n_dies (co-locates ACCs only when #groups is a multiple of
+ *        the die count).
  *
  * The result does not depend on the mapping, bit for bit.
  *
@@ -56,12 +60,13 @@ extern "C" {
 typedef enum {
   ATTN_MAP_BLOCK_FIRST = 0,         /* PAPER.md:226 */
   ATTN_MAP_HEAD_FIRST = 1,          /* PAPER.md:246 */
-  ATTN_MAP_SWIZZLED_HEAD_FIRST = 2  /* PAPER.md:259-304 */
+  ATTN_MAP_SWIZZLED_HEAD_FIRST = 2, /* PAPER.md:259-304 */
+  ATTN_MAP_SWIZZLED_BLOCK_FIRST = 3 /* PAPER.md:236-243, SPEC.md:172 */
 } attn_mapping_t;
 
 typedef enum {
   ATTN_OK = 0,
-  ATTN_ERR_INVALID_VALUE = 1, /* null pointer, size <= 0, Hq % Hkv != 0, bad mapping,
+  ATTN_ERR_INVALID_VALUE = 1, /* null pointer, size <= 0, Hq % Hkv != 0, mapping not in 0..3,
                                  non-finite scale, overlap, not device memory */
   ATTN_ERR_UNSUPPORTED = 2,   /* d not in {64,128}; N % 128 != 0; misaligned; scale < 0;
                                  device is not sm_100 */

@@ -11,6 +11,10 @@ Paper passages (PAPER.md line numbers, "P:n"; SPEC.md lines "S:n"):
   P:206, :220  Attention Compute Cluster (ACC): one head (MHA) / group (GQA)
   P:226        Naive Block-first: all heads of block 0, then block 1, ...
   P:246        Naive Head-first: all blocks of head 0, then head 1, ...
+  P:236-243    Swizzled Block-first (AITER): block-first order with GQA groups
+               pinned to XCDs; keeps locality only when #groups == #XCDs
+  S:172        SwizzledBlockFirst: groups with kv_group mod X == x go to XCD x,
+               enumerated block-major within the XCD's queue
   P:259-304    Swizzled Head-first: each head's blocks on one die; each die
                serves one ACC at a time; fig:head-first-code (Fig. 7)
   S:55         kv_group = q_head // (H_Q / H_K)
@@ -35,7 +39,8 @@ Tile = Tuple[int, int, int]  # (b, h, blk)
 BLOCK_FIRST = "block_first"
 HEAD_FIRST = "head_first"
 SWIZZLED_HEAD_FIRST = "swizzled_head_first"
-MAPPINGS = (BLOCK_FIRST, HEAD_FIRST, SWIZZLED_HEAD_FIRST)
+SWIZZLED_BLOCK_FIRST = "swizzled_block_first"
+MAPPINGS = (BLOCK_FIRST, HEAD_FIRST, SWIZZLED_HEAD_FIRST, SWIZZLED_BLOCK_FIRST)
 
 
 # ---------------------------------------------------------------- attn-grid
@@ -148,10 +153,24 @@ def build_queues(mapping: str, B: int, Hq: int, Hkv: int, nblk: int,
         return [block_major_tiles(B, Hq, nblk)]
     if mapping == HEAD_FIRST:
         return [head_major_tiles(B, Hq, nblk)]
-    if mapping != SWIZZLED_HEAD_FIRST:
-        raise ValueError(mapping)
     D = len(domain_sizes)
     G = Hq // Hkv
+    if mapping == SWIZZLED_BLOCK_FIRST:
+        # S:172 / P:243: die d serves the KV groups g with g mod D == d, block-major
+        # within its queue (for b: for blk: for its groups' heads).  With one die
+        # this is plain block-first.
+        if D == 1:
+            return [block_major_tiles(B, Hq, nblk)]
+        queues = [[] for _ in range(D)]
+        for d in range(D):
+            groups = [g for g in range(Hkv) if g % D == d]
+            for b in range(B):
+                for k in range(nblk):
+                    for g in groups:
+                        queues[d].extend((b, h, k) for h in range(g * G, (g + 1) * G))
+        return queues
+    if mapping != SWIZZLED_HEAD_FIRST:
+        raise ValueError(mapping)
     if D == 1:
         return [head_major_tiles(B, Hq, nblk)]
     queues: List[List[Tile]] = [[] for _ in range(D)]

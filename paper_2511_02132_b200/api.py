@@ -14,9 +14,9 @@ import torch
 
 from . import _lib
 
-MAPPINGS = {"block_first": 0, "head_first": 1, "swizzled_head_first": 2,
-            "bf": 0, "hf": 1, "shf": 2}
-MAPPING_NAMES = ("block_first", "head_first", "swizzled_head_first")
+MAPPINGS = {"block_first": 0, "head_first": 1, "swizzled_head_first": 2, "swizzled_block_first": 3,
+            "bf": 0, "hf": 1, "shf": 2, "sbf": 3}
+MAPPING_NAMES = ("block_first", "head_first", "swizzled_head_first", "swizzled_block_first")
 
 
 class AttnError(RuntimeError):

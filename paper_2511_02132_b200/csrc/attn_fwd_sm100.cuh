@@ -36,6 +36,12 @@ namespace attn {
 
 constexpr int kBlockM = 128;  // query rows per tile (the paper's BLOCK_M)
 constexpr int kBlockN = 128;  // keys per K/V block
+#ifndef ATTN_KV_EVICT_LAST
+#define ATTN_KV_EVICT_LAST 0
+#endif
+#ifndef ATTN_O_EVICT_FIRST
+#define ATTN_O_EVICT_FIRST 0
+#endif
 #ifndef ATTN_SPLIT
 #define ATTN_SPLIT 1
 #endif
@@ -72,11 +78,14 @@ struct Cfg {
   static constexpr int kChunks = D / 64;                  // 128-byte swizzle atoms per row
   static constexpr int kQTileBytes = kBlockM * D * 2;     // one 128-row Q tile
   static constexpr int kKVBytes = kBlockN * D * 2;        // one K or V block
-  static constexpr int kStages = (D == 128) ? 4 : 8;      // K/V ring slots
+#ifndef ATTN_KV_STAGES
+#define ATTN_KV_STAGES 4
+#endif
+  static constexpr int kStages = (D == 128) ? ATTN_KV_STAGES : 8;  // K/V ring slots
   static constexpr int kOffQ = 0;
   static constexpr int kOffKV = 2 * kQTileBytes;
   static constexpr int kOffCtrl = kOffKV + kStages * kKVBytes;
-  static constexpr int kCtrlBytes = 8192;
+  static constexpr int kCtrlBytes = (kSplit == 1) ? 1024 : 8192;
   static constexpr int kSmemBytes = kOffCtrl + kCtrlBytes + 1024;  // + alignment slack
   // TMEM columns: S_t at 128*t, O_t at 256 + D*t
   static __device__ __forceinline__ uint32_t col_s(int t) { return 128u * t; }
@@ -106,6 +115,9 @@ struct __align__(16) Ctrl {
   uint64_t o_ready[2];
   int4 entry[kSchedRing];  // (b, h, u, valid)
   uint32_t tmem_base;
+};
+// cross-warp row reductions of the kSplit == 2 softmax (after Ctrl in SMEM)
+struct SplitRed {
   float red[2][4][2][2][32];   // [tile][quarter][half][parity][lane] partial row max
   float lsum[2][4][2][32];     // [tile][quarter][half][lane] partial row sum (epilogue)
 };
@@ -146,6 +158,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* q_smem = smem + C::kOffQ;
   uint8_t* kv_smem = smem + C::kOffKV;
   Ctrl* ctrl = reinterpret_cast<Ctrl*>(smem + C::kOffCtrl);
+  [[maybe_unused]] SplitRed* sred = reinterpret_cast<SplitRed*>(smem + C::kOffCtrl + 1024);
+  static_assert(sizeof(Ctrl) <= 1024, "control block exceeds 1 KB");
+  static_assert(kSplit == 1 || C::kCtrlBytes >= 1024 + (int)sizeof(SplitRed), "split reductions do not fit");
+  static_assert(C::kSmemBytes <= 232448, "shared memory exceeds 227 KB");
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -188,7 +204,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       SchedReader sr;
       const uint64_t pol_q = ptx::policy_evict_first();
+#if ATTN_KV_EVICT_LAST
+      const uint64_t pol_kv = ptx::policy_evict_last();
+#else
       const uint64_t pol_kv = ptx::policy_evict_normal();
+#endif
       uint32_t q_phase = 0;
       int kv_stage = 0;
       uint32_t kv_phase = 0;
@@ -409,6 +429,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t colO = C::col_o(t) + hf * kOCols;
     [[maybe_unused]] const uint32_t bar_id = 1 + t * 4 + quarter;  // named barrier of the row group's warps
     const float c = p.scale_log2;
+#if ATTN_O_EVICT_FIRST
+    const uint64_t pol_o = ptx::policy_evict_first();
+#endif
     SchedReader sr;
     uint32_t s_phase = 0, o_phase = 0, gblk = 0;
     while (true) {
@@ -452,9 +475,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
         if constexpr (kSplit == 2) {
-          ctrl->red[t][quarter][hf][gblk & 1][lane] = mx;
+          sred->red[t][quarter][hf][gblk & 1][lane] = mx;
           ptx::named_bar_sync(bar_id, 64);
-          mx = fmaxf(mx, ctrl->red[t][quarter][hf ^ 1][gblk & 1][lane]);
+          mx = fmaxf(mx, sred->red[t][quarter][hf ^ 1][gblk & 1][lane]);
         }
         float m_use, alpha;
         bool rescale = false;
@@ -522,9 +545,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       // ---- epilogue: O / l -> bf16 -> global
       if constexpr (kSplit == 2) {
-        ctrl->lsum[t][quarter][hf][lane] = l;
+        sred->lsum[t][quarter][hf][lane] = l;
         ptx::named_bar_sync(bar_id, 64);
-        l += ctrl->lsum[t][quarter][hf ^ 1][lane];
+        l += sred->lsum[t][quarter][hf ^ 1][lane];
       }
       ptx::mbar_wait(&ctrl->o_ready[t], o_phase);
       o_phase ^= 1;
@@ -541,8 +564,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int k = 0; k < 16; ++k)
           pk[k] = ptx::pack_bf16(__uint_as_float(o[2 * k]) * inv_l, __uint_as_float(o[2 * k + 1]) * inv_l);
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
+        for (int k = 0; k < 4; ++k) {
+#if ATTN_O_EVICT_FIRST
+          ptx::st_global_v4_evict_first(dst + cc / 8 + k, make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]), pol_o);
+#else
           dst[cc / 8 + k] = make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
+#endif
+        }
       }
       ptx::tc_fence_before();
     }

@@ -13,6 +13,9 @@
 //   kind 2  per-batch head range (Swizzled Head-first, Fig. 7 with
 //           batch outermost): queue d holds, for every b, heads
 //           [h_lo, h_lo + h_cnt) (whole ACCs) in head-major order.
+//   kind 3  strided groups, block-major (Swizzled Block-first, P:236-243,
+//           S:172): queue d holds the KV groups g = h_lo + i*stride
+//           (i < n_groups) in order for b, for u, for g, for the G heads of g.
 // Block-first and head-first use ONE queue popped by every SM of every die;
 // swizzled head-first uses one queue per die (reading R8).
 #pragma once
@@ -31,11 +34,13 @@ namespace attn {
 constexpr int kMaxQueues = 8;
 
 struct QueueDesc {
-  int kind;   // 0 block-major range, 1 head-major range, 2 per-batch head range
-  int start;  // first position (kinds 0, 1)
-  int len;    // number of units in the queue
-  int h_lo;   // kind 2: first query head
-  int h_cnt;  // kind 2: number of query heads per batch item
+  int kind;    // 0 block-major range, 1 head-major range, 2 per-batch head range, 3 strided groups
+  int start;   // first position (kinds 0, 1)
+  int len;     // number of units in the queue
+  int h_lo;    // kind 2: first query head; kind 3: first KV group
+  int h_cnt;   // kind 2: query heads per batch item; kind 3: number of KV groups
+  int stride;  // kind 3: KV-group stride (= number of dies)
+  int G;       // kind 3: query heads per KV group
 };
 
 struct SchedParams {
@@ -57,12 +62,19 @@ ATTN_HD void decode_unit(const QueueDesc& qd, int pos, int Hq, int U, int& b, in
     b = hm / (Hq * U);
     h = (hm / U) % Hq;
     u = hm % U;
-  } else {
+  } else if (qd.kind == 2) {
     const int per_b = qd.h_cnt * U;
     b = pos / per_b;
     const int r = pos % per_b;
     h = qd.h_lo + r / U;
     u = r % U;
+  } else {
+    const int per_u = qd.h_cnt * qd.G;  // units of one (b, u) row of the queue
+    b = pos / (per_u * U);
+    const int r = pos % (per_u * U);
+    u = r / per_u;
+    const int i = r % per_u;
+    h = (qd.h_lo + (i / qd.G) * qd.stride) * qd.G + i % qd.G;
   }
 }
 
@@ -75,7 +87,7 @@ inline int prop_cut(long long total, const int* sizes, int n, int d) {
   return (int)((total * acc + S / 2) / S);
 }
 
-// Build the queues of `mapping` (0 BF, 1 HF, 2 SHF) for n_domains dies.
+// Build the queues of `mapping` (0 BF, 1 HF, 2 SHF, 3 SBF) for n_domains dies.
 // Returns false on bad arguments.
 inline bool build_sched(int mapping, int B, int Hq, int Hkv, int U, int n_domains, const int* sms_per_domain,
                         SchedParams& sp) {
@@ -84,32 +96,40 @@ inline bool build_sched(int mapping, int B, int Hq, int Hkv, int U, int n_domain
   if (n_domains < 1 || n_domains > kMaxQueues) return false;
   const int G = Hq / Hkv;
   const int total = B * Hq * U;
+  if (mapping < 0 || mapping > 3) return false;
   if (mapping == 0 || mapping == 1 || n_domains == 1) {
+    const bool block_major = (mapping == 0 || mapping == 3);  // SBF on one die == BF
     sp.n_queues = 1;
     sp.steal = 0;
-    sp.q[0] = QueueDesc{mapping == 0 ? 0 : 1, 0, total, 0, Hq};
-    return mapping >= 0 && mapping <= 2;
+    sp.q[0] = QueueDesc{block_major ? 0 : 1, 0, total, 0, Hq, 0, 0};
+    return true;
   }
-  if (mapping != 2) return false;
   const int D = n_domains;
   sp.n_queues = D;
   sp.steal = 1;
   for (int d = 0; d < D; ++d) sp.queue_of_domain[d] = d;
+  if (mapping == 3) {
+    for (int d = 0; d < D; ++d) {
+      const int ng = (Hkv > d) ? (Hkv - d + D - 1) / D : 0;  // groups g = d, d + D, ...
+      sp.q[d] = QueueDesc{3, 0, B * U * ng * G, d, ng, D, G};
+    }
+    return true;
+  }
   if (Hkv >= D) {
     for (int d = 0; d < D; ++d) {
       const int a0 = prop_cut(Hkv, sms_per_domain, D, d), a1 = prop_cut(Hkv, sms_per_domain, D, d + 1);
-      sp.q[d] = QueueDesc{2, 0, B * (a1 - a0) * G * U, a0 * G, (a1 - a0) * G};
+      sp.q[d] = QueueDesc{2, 0, B * (a1 - a0) * G * U, a0 * G, (a1 - a0) * G, 0, 0};
     }
   } else if ((long long)B * Hkv >= D) {
     const int A = B * Hkv;
     for (int d = 0; d < D; ++d) {
       const int a0 = prop_cut(A, sms_per_domain, D, d), a1 = prop_cut(A, sms_per_domain, D, d + 1);
-      sp.q[d] = QueueDesc{1, a0 * G * U, (a1 - a0) * G * U, 0, Hq};
+      sp.q[d] = QueueDesc{1, a0 * G * U, (a1 - a0) * G * U, 0, Hq, 0, 0};
     }
   } else {
     for (int d = 0; d < D; ++d) {
       const int t0 = prop_cut(total, sms_per_domain, D, d), t1 = prop_cut(total, sms_per_domain, D, d + 1);
-      sp.q[d] = QueueDesc{1, t0, t1 - t0, 0, Hq};
+      sp.q[d] = QueueDesc{1, t0, t1 - t0, 0, Hq, 0, 0};
     }
   }
   return true;

@@ -134,3 +134,20 @@ def test_repeated_launches_self_reset_counters():
         o = attn_fwd(q, k, v, causal=False, mapping="swizzled_head_first")
     torch.cuda.synchronize()
     assert torch.equal(o.view(torch.int16), ref.view(torch.int16))
+
+
+def test_swizzled_block_first_pins_groups_to_dies():
+    """P:243: with #groups a multiple of the die count, SBF keeps every GQA
+    group (ACC) on one die (apart from tail steals)."""
+    t = attn_topology(0)
+    if t["n_domains"] < 2:
+        pytest.skip("probe found one domain")
+    B, Hq, Hkv, N, d = 2, 32, 8, 4096, 128
+    tr, _ = _trace_run(B, Hq, Hkv, N, d, True, "swizzled_block_first")
+    G = Hq // Hkv
+    dom_of_acc = collections.defaultdict(set)
+    for b, h, u, sm, dom, qi, st, seq in tr.tolist():
+        if not st:
+            dom_of_acc[(b, h // G)].add(dom)
+            assert (h // G) % t["n_domains"] == qi
+    assert all(len(s) == 1 for s in dom_of_acc.values())

@@ -157,6 +157,22 @@ def test_random_configs_bijective_and_colocated():
             assert key == sorted(key)
 
 
+def test_swizzled_block_first_examples():
+    """groups with g mod X == x on XCD x, block-major inside; with
+    #groups == #dies every ACC sits on one die."""
+    q = om.build_queues("swizzled_block_first", 1, 8, 2, 3, [74, 74])   # GQA, 2 groups of 4
+    assert q[0] == [(0, h, k) for k in range(3) for h in range(4)]
+    assert q[1] == [(0, h, k) for k in range(3) for h in range(4, 8)]
+    mha = om.build_queues("swizzled_block_first", 1, 4, 4, 2, [74, 74])
+    assert mha[0] == [(0, 0, 0), (0, 2, 0), (0, 0, 1), (0, 2, 1)]
+    assert mha[1] == [(0, 1, 0), (0, 3, 0), (0, 1, 1), (0, 3, 1)]
+    for Hkv in (2, 8):
+        qs = om.build_queues("swizzled_block_first", 2, 64, Hkv, 4, [74, 74])
+        assert all(len(s) == 1 for s in om.acc_domains(qs, 64, Hkv).values())
+    assert (om.build_queues("swizzled_block_first", 2, 8, 2, 3, [148])
+            == om.build_queues("block_first", 2, 8, 2, 3, [148]))
+
+
 def test_single_domain_degenerates_to_head_first():
     """S:189 / S:206: with one die SHF == HF."""
     for B, Hq, Hkv, nblk in ((1, 4, 4, 3), (2, 8, 2, 5)):
