@@ -235,6 +235,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int which = 0; which < 2; ++which) {
             ptx::mbar_wait(&ctrl->kv_empty[kv_stage], kv_phase ^ 1);
+      #ifdef ATTN_DEBUG_NO_KV_LOAD
+            if (j >= 2) {  // bandwidth probe: reuse whatever is in the slot
+              ptx::mbar_arrive(&ctrl->kv_full[kv_stage]);
+              if (++kv_stage == C::kStages) { kv_stage = 0; kv_phase ^= 1; }
+              continue;
+            }
+#endif
             ptx::mbar_arrive_expect_tx(&ctrl->kv_full[kv_stage], C::kKVBytes);
             uint8_t* dst = kv_smem + kv_stage * C::kKVBytes;
 #pragma unroll
@@ -254,7 +261,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(&ctrl->tmem_base);
     SchedReader sr;
     constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(kBlockM, kBlockN, 0, 0);
+#ifdef ATTN_DEBUG_PV_KMAJOR
+    constexpr uint32_t idesc_o = ptx::idesc_bf16_f32(kBlockM, D, 0, 0);  // wrong layout: speed probe only
+#else
     constexpr uint32_t idesc_o = ptx::idesc_bf16_f32(kBlockM, D, 0, 1);
+#endif
     // descriptors at k = 0; advancing K by 16 elements adds 32 B (2 in the
     // >>4 address field) inside a 128-byte swizzle atom, and one atom
     // (rows * 128 B) every 4 steps.
@@ -262,6 +273,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t dkv0 = ptx::smem_desc_sw128(ptx::smem_u32(kv_smem), 16, 1024);
     const uint64_t dv0 = ptx::smem_desc_sw128(ptx::smem_u32(kv_smem), kBlockN * 128, 1024);
     uint32_t q_phase = 0, p_phase0 = 0, p_phase1 = 0;
+    [[maybe_unused]] int unit_no = -1;
     int kv_stage = 0;
     uint32_t kv_phase = 0;
 
@@ -269,12 +281,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t dq = dq0 + (uint64_t)((t * C::kQTileBytes) >> 4);
       const uint64_t dk = dkv0 + (uint64_t)((slot * C::kKVBytes) >> 4);
       const uint32_t d_tmem = tmem + C::col_s(t);
+#ifndef ATTN_DEBUG_NO_S
 #pragma unroll
       for (int k = 0; k < D / 16; ++k) {
         const uint32_t oq = ((k >> 2) * (kBlockM * 128) + (k & 3) * 32) >> 4;
         const uint32_t ok = ((k >> 2) * (kBlockN * 128) + (k & 3) * 32) >> 4;
         ptx::mma_ss(d_tmem, dq + oq, dk + ok, idesc_s, k > 0 ? 1u : 0u);
       }
+#endif
     };
     // O_t += P_t V: K = 128 keys in 8 steps of 16; steps [4h, 4h+4) read the
     // half h of P, which the softmax publishes separately (p_ready[t][h]).
@@ -282,27 +296,38 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t dv = dv0 + (uint64_t)((slot * C::kKVBytes) >> 4);
       const uint32_t d_tmem = tmem + C::col_o(t);
       const uint32_t a_tmem = tmem + C::col_s(t);
+#ifndef ATTN_DEBUG_NO_PV
 #pragma unroll
       for (int k = 4 * h; k < 4 * h + 4; ++k)
         ptx::mma_ts(d_tmem, a_tmem + k * 8, dv + (uint64_t)((k * 16 * 128) >> 4), idesc_o,
                     (acc || k > 0) ? 1u : 0u);
+#endif
     };
+#ifdef ATTN_PROFILE_WAITS
+    long long w_q = 0, w_kv = 0, w_p0 = 0, w_p1 = 0, w_sched = 0;
+    const long long t_start = clock64();
+#define ATTN_TIMED(acc, stmt) { const long long t0_ = clock64(); stmt; acc += clock64() - t0_; }
+#else
+#define ATTN_TIMED(acc, stmt) stmt;
+#endif
     auto take_slot = [&]() {
       const int s = kv_stage;
-      ptx::mbar_wait(&ctrl->kv_full[s], kv_phase);
+      ATTN_TIMED(w_kv, ptx::mbar_wait(&ctrl->kv_full[s], kv_phase));
       if (++kv_stage == C::kStages) { kv_stage = 0; kv_phase ^= 1; }
       return s;
     };
 
     while (true) {
-      const int4 e = sr.next(ctrl, false);
+      int4 e;
+      ATTN_TIMED(w_sched, e = sr.next(ctrl, false));
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&ctrl->sched_empty[(sr.stage + kSchedRing - 1) % kSchedRing]);
       if (!e.w) break;
       int n0, n1;
       unit_blocks<kCausal>(e.z, p.nblk, n0, n1);
       const int n = n0 > n1 ? n0 : n1;
-      ptx::mbar_wait(&ctrl->q_full, q_phase);
+      ATTN_TIMED(w_q, ptx::mbar_wait(&ctrl->q_full, q_phase));
+      ++unit_no;
       q_phase ^= 1;
       int sK = take_slot();
       ptx::tc_fence_after();
@@ -319,10 +344,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (n == 1) ptx::mma_commit(&ctrl->q_empty);
       }
       __syncwarp();
+#ifdef ATTN_TIMELINE
+      long long* tl = (p.trace && blockIdx.x == 0) ? reinterpret_cast<long long*>(p.trace) : nullptr;
+      if (tl && lane == 0) tl[1000] = clock64();
+#define ATTN_STAMP(i) if (tl && lane == 0 && j < 64 && unit_no == 0) tl[j * 8 + (i)] = clock64();
+#else
+#define ATTN_STAMP(i)
+#endif
       for (int j = 0; j < n; ++j) {
+        ATTN_STAMP(0);
         const int sV = take_slot();
         const bool nxt = j + 1 < n;
         if (nxt) sK = take_slot();
+        ATTN_STAMP(1);
         ptx::tc_fence_after();
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
@@ -331,7 +365,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t ph = (t == 0) ? p_phase0 : p_phase1;
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-              ptx::mbar_wait(&ctrl->p_ready[t][h], ph);
+              if (t == 0) { ATTN_TIMED(w_p0, ptx::mbar_wait(&ctrl->p_ready[t][h], ph)); }
+              else { ATTN_TIMED(w_p1, ptx::mbar_wait(&ctrl->p_ready[t][h], ph)); }
+              if (h == 1) { ATTN_STAMP(2 + 2 * t); }
               ptx::tc_fence_after();
               if (ptx::elect_one_sync()) issue_pv_half(t, sV, j > 0, h);
               __syncwarp();
@@ -346,6 +382,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
             __syncwarp();
+            ATTN_STAMP(3 + 2 * t);
           }
         }
         if (ptx::elect_one_sync()) {
@@ -358,6 +395,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
       }
     }
+#ifdef ATTN_PROFILE_WAITS
+    if (lane == 0 && p.trace) {
+      long long* out = reinterpret_cast<long long*>(p.trace) + blockIdx.x * 8;
+      out[0] = clock64() - t_start; out[1] = w_q; out[2] = w_kv; out[3] = w_p0; out[4] = w_p1; out[5] = w_sched;
+    }
+#endif
   } else if (warp == 2) {
     // --------------------------------------------------------------- scheduler
     if (ATTN_SETMAXNREG) ptx::setmaxnreg_dec<kOtherRegs>();
@@ -390,6 +433,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ctrl->entry[stage] = make_int4(b, h, u, qi >= 0 ? 1 : 0);
         ptx::mbar_arrive(&ctrl->sched_full[stage]);
         if (qi < 0) break;
+#ifndef ATTN_PROFILE_WAITS
         if (p.trace) {
           const long long id = ((long long)b * p.Hq + h) * p.U + u;
           if (id < p.trace_cap) {
@@ -399,6 +443,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             p.trace[id] = r;
           }
         }
+#endif
         ++seq;
         if (++stage == kSchedRing) { stage = 0; phase ^= 1; }
       }
@@ -445,11 +490,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (nt == 0) continue;
       const int qb = 2 * e.z + t;
       const int lim = row - cbase;  // diagonal block: local key k visible iff k <= lim
+#ifdef ATTN_TIMELINE
+      const bool first_unit = (gblk == 0);
+#endif
       float m = -INFINITY, l = 0.f;
       for (int j = 0; j < nt; ++j, ++gblk) {
         ptx::mbar_wait(&ctrl->s_ready[t], s_phase);
         s_phase ^= 1;
         ptx::tc_fence_after();
+#ifdef ATTN_TIMELINE
+        long long* tls = (p.trace && blockIdx.x == 0 && quarter == 0 && lane == 0 && first_unit && j < 64)
+                             ? reinterpret_cast<long long*>(p.trace) + 600 + t * 200 + j * 3 : nullptr;
+        if (tls) tls[0] = clock64();
+#endif
 #ifdef ATTN_DEBUG_SKIP_SOFTMAX
         __syncwarp();
         if (lane == 0) { ptx::mbar_arrive(&ctrl->p_ready[t][0]); ptx::mbar_arrive(&ctrl->p_ready[t][1]); }
@@ -536,6 +589,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&ctrl->p_ready[t][h]);
+#ifdef ATTN_TIMELINE
+          if (tls) tls[1 + h] = clock64();
+#endif
         }
         const float2 s01 = ptx::fadd2(sq[0], sq[1]), s23 = ptx::fadd2(sq[2], sq[3]);
         const float2 s4 = ptx::fadd2(s01, s23);

@@ -1,0 +1,31 @@
+"""Per-iteration timeline of CTA 0 (build with -D ATTN_TIMELINE)."""
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from paper_2511_02132_b200 import attn_fwd, attn_set_schedule_trace, synth
+
+q, k, v = synth.make_qkv(1, 32, 32, 8192, 128, base=0, device="cuda")
+attn_fwd(q, k, v)
+buf = torch.zeros(2048 * 2, dtype=torch.int32, device="cuda")
+attn_set_schedule_trace(0, buf)
+attn_fwd(q, k, v, mapping="swizzled_head_first")
+torch.cuda.synchronize()
+attn_set_schedule_trace(0, None)
+t = buf.view(torch.int64).cpu().numpy().astype(np.int64)
+t0 = t[1000]
+mma = t[:64 * 8].reshape(64, 8)[:, :6] - t0
+sm0 = t[600:600 + 192].reshape(64, 3) - t0
+sm1 = t[800:800 + 192].reshape(64, 3) - t0
+print(" j | it_start  kv_ok  p0_ok  t0_iss  p1_ok  t1_iss | sm0: s_wake  p_h0  p_h1 | sm1: s_wake  p_h0  p_h1")
+for j in range(8, 24):
+    print(f"{j:2d} | " + " ".join(f"{x:7d}" for x in mma[j]) + " | " + " ".join(f"{x:6d}" for x in sm0[j]) +
+          " | " + " ".join(f"{x:6d}" for x in sm1[j]))
+d = np.diff(mma[8:60, 0])
+print("cycles per iteration (median over j=8..60):", int(np.median(d)), " ideal 2048")
+print("softmax0 s_wake -> p_h1 (median):", int(np.median(sm0[8:60, 2] - sm0[8:60, 0])),
+      " softmax1:", int(np.median(sm1[8:60, 2] - sm1[8:60, 0])))
+print("t0 issue done -> softmax0 next s_wake (median):", int(np.median(sm0[9:61, 0] - mma[8:60, 3])))
+print("softmax0 p_h1 -> MMA p0_ok (median):", int(np.median(mma[9:61, 2] - sm0[9:61, 2])))
