@@ -144,15 +144,17 @@ def run_ours(a):
     # enough to survive in L2 between steps (no flush inside the timed region)
     l2 = topo["l2_bytes"]
     set_bytes = 2 * B * (2 * hq + 2 * hkv) * N * d
-    n_sets = 1 if set_bytes > 4 * l2 else 3
+    n_sets = a.sets if a.sets > 0 else (1 if set_bytes > 4 * l2 else 3)
     sets = []
     for s in range(n_sets):
         q, k, v = synth.make_qkv(B, hq, hkv, N, d, base=s, q_head_offset=shard.q_lo, kv_head_offset=shard.kv_lo,
                                  device=dev)
         sets.append((q, k, v, torch.empty_like(q)))
     l2_note = (f"inputs rotated over {n_sets} sets ({n_sets * set_bytes / 2**20:.0f} MiB > L2 "
-               f"{l2 / 2**20:.0f} MiB); no flush" if n_sets > 1 else
-               f"one input set of {set_bytes / 2**20:.0f} MiB > L2 {l2 / 2**20:.0f} MiB; no flush")
+               f"{l2 / 2**20:.0f} MiB)" if n_sets > 1 else
+               f"one input set of {set_bytes / 2**20:.0f} MiB (L2 {l2 / 2**20:.0f} MiB)")
+    l2_note += "; L2 flushed (memset 2xL2) before every step, outside the per-launch events" if a.flush else "; no flush"
+    flush_buf = torch.empty(2 * l2, dtype=torch.uint8, device=dev) if a.flush else None
     stream = torch.cuda.current_stream()
     flops_rank = flops_fwd(B, hq, N, d, causal)
     flops_job = flops_fwd(B, Hq_job, N, d, causal)
@@ -175,6 +177,8 @@ def run_ours(a):
         with ctx:
             e0.record(stream)
             for i in range(steps):
+                if flush_buf is not None:
+                    flush_buf.zero_()
                 evs[i][0].record(stream)
                 step(i, mapping)
                 evs[i][1].record(stream)
@@ -368,6 +372,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--sets", type=int, default=0, help="resident input sets rotated per step (0: auto)")
+    ap.add_argument("--flush", action="store_true", help="memset a 2xL2 buffer before every step")
     a = ap.parse_args()
     if a.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

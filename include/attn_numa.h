@@ -30,6 +30,9 @@
  *    all bf16 (raw 16-bit storage, passed as void*).  Accumulation is fp32.
  *  - GQA grouping: query head h reads K/V head h / (Hq / Hkv).
  *  - causal != 0 masks key j from query i when j > i (N_q == N_k).
+ *  - Head dim d: any multiple of 8 up to 128 (DeepSeek-V3's 56, PAPER.md:417,
+ *    included).  The kernel runs at 64 or 128 columns; TMA zero-fills the
+ *    padding columns on load and they are never stored.
  *  - Pointers of attn_fwd / attn_fwd_stream are DEVICE pointers on the
  *    calling thread's current CUDA device; the caller owns them.  The
  *    library never frees or retains them beyond the enqueued kernel; q, k, v
@@ -68,7 +71,7 @@ typedef enum {
   ATTN_OK = 0,
   ATTN_ERR_INVALID_VALUE = 1, /* null pointer, size <= 0, Hq % Hkv != 0, mapping not in 0..3,
                                  non-finite scale, overlap, not device memory */
-  ATTN_ERR_UNSUPPORTED = 2,   /* d not in {64,128}; N % 128 != 0; misaligned; scale < 0;
+  ATTN_ERR_UNSUPPORTED = 2,   /* d > 128 or d % 8 != 0; N % 128 != 0; misaligned; scale < 0;
                                  device is not sm_100 */
   ATTN_ERR_CUDA = 3,          /* CUDA runtime / driver failure (see attn_last_error) */
   ATTN_ERR_TOPOLOGY = 4       /* the die probe itself failed (an inconclusive probe is

@@ -341,7 +341,7 @@ int validate(const void* q, const void* k, const void* v, void* o, int B, int Hq
   const size_t qb = (size_t)B * Hq * N * d * 2, kb = (size_t)B * Hkv * N * d * 2;
   if (overlaps(o, qb, q, qb) || overlaps(o, qb, k, kb) || overlaps(o, qb, v, kb))
     return fail(ATTN_ERR_INVALID_VALUE, "o overlaps an input");
-  if (d != 64 && d != 128) return fail(ATTN_ERR_UNSUPPORTED, "head dim must be 64 or 128");
+  if (d > 128 || d % 8 != 0) return fail(ATTN_ERR_UNSUPPORTED, "head dim must be a multiple of 8 and <= 128");
   if (N % 128 != 0) return fail(ATTN_ERR_UNSUPPORTED, "N must be a multiple of 128");
   if (scale < 0.f) return fail(ATTN_ERR_UNSUPPORTED, "negative scale");
   if ((long long)B * Hq * N >= (1ll << 31) || (long long)B * Hkv * N >= (1ll << 31))
@@ -403,6 +403,8 @@ int fwd_impl(const void* q, const void* k, const void* v, void* o, int B, int Hq
   const int U = (nblk + 1) / 2;
   KernelParams kp{};
   kp.B = B; kp.Hq = Hq; kp.Hkv = Hkv; kp.N = N; kp.G = Hq / Hkv; kp.U = U; kp.nblk = nblk;
+  kp.d_real = d;
+  const int dpad = d <= 64 ? 64 : 128;  // kernel head dim; TMA zero-fills columns d..dpad-1
   kp.scale_log2 = scale * 1.4426950408889634f;
   kp.o = reinterpret_cast<__nv_bfloat16*>(o);
   if (!build_sched(mapping, B, Hq, Hkv, U, st.active.n_domains, st.active.sms_per_domain, kp.sched))
@@ -421,8 +423,8 @@ int fwd_impl(const void* q, const void* k, const void* v, void* o, int B, int Hq
 
   const int total = B * Hq * U;
   const int grid = std::min(st.num_sms, total);
-  if (d == 128 && causal) rc = launch_t<128, true>(st, 0, tq, tk, tv, kp, grid, stream);
-  else if (d == 128) rc = launch_t<128, false>(st, 1, tq, tk, tv, kp, grid, stream);
+  if (dpad == 128 && causal) rc = launch_t<128, true>(st, 0, tq, tk, tv, kp, grid, stream);
+  else if (dpad == 128) rc = launch_t<128, false>(st, 1, tq, tk, tv, kp, grid, stream);
   else if (causal) rc = launch_t<64, true>(st, 2, tq, tk, tv, kp, grid, stream);
   else rc = launch_t<64, false>(st, 3, tq, tk, tv, kp, grid, stream);
   if (rc != ATTN_OK) return rc;

@@ -42,6 +42,9 @@ constexpr int kBlockN = 128;  // keys per K/V block
 #ifndef ATTN_O_EVICT_FIRST
 #define ATTN_O_EVICT_FIRST 0
 #endif
+#ifndef ATTN_EXP_F16X2
+#define ATTN_EXP_F16X2 0
+#endif
 #ifndef ATTN_SPLIT
 #define ATTN_SPLIT 1
 #endif
@@ -94,6 +97,7 @@ struct Cfg {
 
 struct KernelParams {
   int B, Hq, Hkv, N, G, U, nblk;
+  int d_real;        // head dim of the tensors (<= D; TMA zero-fills columns d_real..D-1)
   float scale_log2;  // scale * log2(e), >= 0
   __nv_bfloat16* o;
   SchedParams sched;
@@ -573,8 +577,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (kEmuPeriod > 0 && ((k >> 1) % (kEmuPeriod > 0 ? kEmuPeriod : 1)) == kEmuPeriod - 1) {
               pr = ptx::ex2_poly2(x);
             } else {
+#if ATTN_EXP_F16X2
+              pr = ptx::ex2_f16x2(x);
+#else
               pr.x = ptx::ex2(x.x);
               pr.y = ptx::ex2(x.y);
+#endif
             }
             if (diag) {
               pr.x = (k <= lim) ? pr.x : 0.f;
@@ -609,8 +617,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       o_phase ^= 1;
       ptx::tc_fence_after();
       const float inv_l = 1.f / l;
-      const long long orow = ((long long)(e.x * p.Hq + e.y) * p.N + (long long)qb * kBlockM + row) * D;
+      const long long orow = ((long long)(e.x * p.Hq + e.y) * p.N + (long long)qb * kBlockM + row) * p.d_real;
       uint4* dst = reinterpret_cast<uint4*>(p.o + orow + hf * kOCols);
+      const int ncol = p.d_real - hf * kOCols;  // real columns of this thread's slice (multiple of 8)
 #pragma unroll
       for (int cc = 0; cc < kOCols; cc += 32) {
         uint32_t o[32];
@@ -621,6 +630,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           pk[k] = ptx::pack_bf16(__uint_as_float(o[2 * k]) * inv_l, __uint_as_float(o[2 * k + 1]) * inv_l);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
+          if (cc + 8 * k >= ncol) break;  // padded head dim: the zero columns are not stored
 #if ATTN_O_EVICT_FIRST
           ptx::st_global_v4_evict_first(dst + cc / 8 + k, make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]), pol_o);
 #else

@@ -348,6 +348,23 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
   return d;
 }
 
+// exp2 of a pair on the MUFU unit at half precision: one MUFU.EX2 on f16x2
+// computes both lanes.  x is rounded to f16 first (|x| <= 16: abs. error
+// <= 2^-7, relative error of 2^x <= 0.5%; |x| <= 1: <= 2^-11); the f16 result
+// is widened exactly to f32.  -inf -> +0, 0 -> 1 exactly.
+__device__ __forceinline__ float2 ex2_f16x2(float2 x) {
+  float2 r;
+  asm("{\n\t.reg .b32 h, e;\n\t.reg .b16 lo, hi;\n\t"
+      "cvt.rn.f16x2.f32 h, %3, %2;\n\t"
+      "ex2.approx.f16x2 e, h;\n\t"
+      "mov.b32 {lo, hi}, e;\n\t"
+      "cvt.f32.f16 %0, lo;\n\t"
+      "cvt.f32.f16 %1, hi;\n\t}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(x.x), "f"(x.y));
+  return r;
+}
+
 // ex2_poly on a pair with packed math (see ex2_poly for the method).
 __device__ __forceinline__ float2 ex2_poly2(float2 x) {
   x.x = fmaxf(x.x, -127.f);

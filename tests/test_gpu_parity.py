@@ -49,6 +49,10 @@ SMALL = [
     (1, 3, 3, 640, 128, False),   # 5 blocks per head, odd head count
     (2, 8, 2, 512, 128, True),
     (1, 4, 1, 1024, 64, True),    # MQA
+    (1, 4, 4, 512, 56, True),     # DeepSeek-V3 head dim, zero-padded to 64 by TMA
+    (2, 4, 2, 384, 96, False),    # padded to 128
+    (1, 2, 2, 256, 8, True),      # smallest head dim
+    (1, 2, 1, 640, 120, True),
 ]
 
 
