@@ -120,11 +120,15 @@ ATTN_API int attn_fwd_stream(const void* q, const void* k, const void* v, void* 
                     int d, int causal, float scale, int mapping, void* cuda_stream);
 
 /* End-to-end variant on HOST buffers (same layout): copies q/k/v host->device
- * into library-owned device buffers, runs attn_fwd_stream, copies o
- * device->host and synchronises the stream before returning.  Host buffers
- * should be pinned (cudaHostAlloc / torch pin_memory) for async copies;
- * pageable memory works but is slower.  Library buffers are reused across
- * calls of equal or smaller size and freed by attn_shutdown(). */
+ * into library-owned device buffers, runs the kernel, copies o device->host
+ * and synchronises `cuda_stream` before returning.  Large problems are split
+ * into chunks of whole KV groups (heads are independent, so the
+ * result is bit-identical to one call) and pipelined on three library streams
+ * ordered after `cuda_stream`: H2D of chunk i+1 overlaps the kernel of chunk i
+ * and the D2H of chunk i-1.  Host buffers should be pinned (cudaHostAlloc /
+ * torch pin_memory) for the copies to overlap; pageable memory works but is
+ * slower.  Library buffers are reused across calls of equal or smaller size
+ * and freed by attn_shutdown().  Not reentrant across threads on one device. */
 ATTN_API int attn_fwd_host(const void* q_host, const void* k_host, const void* v_host, void* o_host, int B, int Hq,
                   int Hkv, int N, int d, int causal, float scale, int mapping, void* cuda_stream);
 

@@ -25,6 +25,7 @@ using namespace attn;
 
 constexpr int kMaxDevices = 16;
 constexpr int kCounterSlots = 64;
+constexpr int kE2EChunks = 8;  // max chunks of the pipelined host-buffer path
 constexpr int kCounterInts = (kMaxQueues + 1) * 32;  // one 128-byte line per queue + done count
 
 thread_local std::string g_err;
@@ -60,6 +61,9 @@ struct DevState {
   // e2e host-buffer path
   void* hbuf[4] = {nullptr, nullptr, nullptr, nullptr};
   size_t hbuf_bytes[4] = {0, 0, 0, 0};
+  bool e2e_ready = false;
+  cudaStream_t e2e_stream[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t e2e_ev[2][kE2EChunks + 1] = {};
 };
 
 DevState g_dev[kMaxDevices];
@@ -452,12 +456,15 @@ int attn_fwd_host(const void* q_host, const void* k_host, const void* v_host, vo
                   int N, int d, int causal, float scale, int mapping, void* cuda_stream) {
   if (!q_host || !k_host || !v_host || !o_host) return fail(ATTN_ERR_INVALID_VALUE, "null pointer");
   if (B <= 0 || Hq <= 0 || Hkv <= 0 || N <= 0 || d <= 0) return fail(ATTN_ERR_INVALID_VALUE, "size <= 0");
+  if (Hq % Hkv != 0) return fail(ATTN_ERR_INVALID_VALUE, "Hq % Hkv != 0 (non-uniform GQA groups)");
   int dev = 0;
   int rc = current_device(dev);
   if (rc != ATTN_OK) return rc;
   DevState& st = g_dev[dev];
   cudaStream_t s = reinterpret_cast<cudaStream_t>(cuda_stream);
-  const size_t nq = (size_t)B * Hq * N * d * 2, nk = (size_t)B * Hkv * N * d * 2;
+  const int G = Hq / Hkv;
+  const size_t row_bytes = (size_t)N * d * 2;  // one head of one batch item
+  const size_t nq = (size_t)B * Hq * row_bytes, nk = (size_t)B * Hkv * row_bytes;
   const size_t need[4] = {nq, nk, nk, nq};
   {
     std::lock_guard<std::mutex> lk(st.mu);
@@ -470,14 +477,55 @@ int attn_fwd_host(const void* q_host, const void* k_host, const void* v_host, vo
         st.hbuf_bytes[i] = need[i];
       }
     }
+    if (!st.e2e_ready) {
+      for (int i = 0; i < 3; ++i) ATTN_CUDA(cudaStreamCreateWithFlags(&st.e2e_stream[i], cudaStreamNonBlocking));
+      for (int i = 0; i < kE2EChunks + 1; ++i)
+        for (int j = 0; j < 2; ++j) ATTN_CUDA(cudaEventCreateWithFlags(&st.e2e_ev[j][i], cudaEventDisableTiming));
+      st.e2e_ready = true;
+    }
   }
-  ATTN_CUDA(cudaMemcpyAsync(st.hbuf[0], q_host, nq, cudaMemcpyHostToDevice, s));
-  ATTN_CUDA(cudaMemcpyAsync(st.hbuf[1], k_host, nk, cudaMemcpyHostToDevice, s));
-  ATTN_CUDA(cudaMemcpyAsync(st.hbuf[2], v_host, nk, cudaMemcpyHostToDevice, s));
-  rc = fwd_impl(st.hbuf[0], st.hbuf[1], st.hbuf[2], st.hbuf[3], B, Hq, Hkv, N, d, causal, scale, mapping, s);
-  if (rc != ATTN_OK) return rc;
-  ATTN_CUDA(cudaMemcpyAsync(o_host, st.hbuf[3], nq, cudaMemcpyDeviceToHost, s));
+  // Chunks of whole KV groups inside one batch item (contiguous sub-tensors;
+  // heads are independent, so the result is bit-identical to one call).
+  // Three-stage pipeline: H2D chunk i+1 || kernel chunk i || D2H chunk i-1.
+  const size_t total = 2 * nq + 2 * nk;
+  int target = (int)std::min<size_t>(kE2EChunks, std::max<size_t>(1, total / (48u << 20)));
+  const int tg = B * Hkv;
+  target = std::min(target, tg);
+  int gpc = (tg + target - 1) / target;  // KV groups per chunk
+  gpc = std::min(gpc, Hkv);
+  cudaStream_t cin = st.e2e_stream[0], comp = st.e2e_stream[1], cout = st.e2e_stream[2];
+  cudaEvent_t* ev_in = st.e2e_ev[0];
+  cudaEvent_t* ev_k = st.e2e_ev[1];
+  ATTN_CUDA(cudaEventRecord(ev_in[kE2EChunks], s));  // order after the caller's prior work
+  for (cudaStream_t x : {cin, comp, cout}) ATTN_CUDA(cudaStreamWaitEvent(x, ev_in[kE2EChunks], 0));
+  char* dq = static_cast<char*>(st.hbuf[0]);
+  char* dk = static_cast<char*>(st.hbuf[1]);
+  char* dv = static_cast<char*>(st.hbuf[2]);
+  char* dout = static_cast<char*>(st.hbuf[3]);
+  int c = 0;
+  for (int b = 0; b < B; ++b) {
+    for (int g0 = 0; g0 < Hkv; g0 += gpc, ++c) {
+      const int gn = std::min(gpc, Hkv - g0);
+      const size_t qoff = ((size_t)b * Hq + (size_t)g0 * G) * row_bytes, qlen = (size_t)gn * G * row_bytes;
+      const size_t koff = ((size_t)b * Hkv + g0) * row_bytes, klen = (size_t)gn * row_bytes;
+      const int e = c % kE2EChunks;
+      if (c >= kE2EChunks) ATTN_CUDA(cudaStreamWaitEvent(cin, ev_k[e], 0));  // slot's previous chunk consumed
+      ATTN_CUDA(cudaMemcpyAsync(dq + qoff, static_cast<const char*>(q_host) + qoff, qlen, cudaMemcpyHostToDevice, cin));
+      ATTN_CUDA(cudaMemcpyAsync(dk + koff, static_cast<const char*>(k_host) + koff, klen, cudaMemcpyHostToDevice, cin));
+      ATTN_CUDA(cudaMemcpyAsync(dv + koff, static_cast<const char*>(v_host) + koff, klen, cudaMemcpyHostToDevice, cin));
+      ATTN_CUDA(cudaEventRecord(ev_in[e], cin));
+      ATTN_CUDA(cudaStreamWaitEvent(comp, ev_in[e], 0));
+      rc = fwd_impl(dq + qoff, dk + koff, dv + koff, dout + qoff, 1, gn * G, gn, N, d, causal, scale, mapping, comp);
+      if (rc != ATTN_OK) return rc;
+      ATTN_CUDA(cudaEventRecord(ev_k[e], comp));
+      ATTN_CUDA(cudaStreamWaitEvent(cout, ev_k[e], 0));
+      ATTN_CUDA(cudaMemcpyAsync(static_cast<char*>(o_host) + qoff, dout + qoff, qlen, cudaMemcpyDeviceToHost, cout));
+    }
+  }
+  ATTN_CUDA(cudaEventRecord(ev_k[kE2EChunks], cout));
+  ATTN_CUDA(cudaStreamWaitEvent(s, ev_k[kE2EChunks], 0));
   ATTN_CUDA(cudaStreamSynchronize(s));
+  g_info.kernel_launches = c;
   return ATTN_OK;
 }
 
@@ -618,6 +666,12 @@ void attn_shutdown(void) {
     st.d_domain = nullptr;
     st.d_counters = nullptr;
     for (int i = 0; i < 4; ++i) { st.hbuf[i] = nullptr; st.hbuf_bytes[i] = 0; }
+    if (st.e2e_ready) {
+      for (int i = 0; i < 3; ++i) cudaStreamDestroy(st.e2e_stream[i]);
+      for (int j = 0; j < 2; ++j)
+        for (int i = 0; i < kE2EChunks + 1; ++i) cudaEventDestroy(st.e2e_ev[j][i]);
+      st.e2e_ready = false;
+    }
     st.init = false;
     for (bool& a : st.attr_done) a = false;
   }

@@ -151,3 +151,17 @@ def test_swizzled_block_first_pins_groups_to_dies():
             dom_of_acc[(b, h // G)].add(dom)
             assert (h // G) % t["n_domains"] == qi
     assert all(len(s) == 1 for s in dom_of_acc.values())
+
+
+def test_host_buffer_pipelined_chunks_bitexact():
+    """Large enough for the chunked H2D / kernel / D2H pipeline (several launches)."""
+    from paper_2511_02132_b200 import attn_last_launch_info
+
+    q, k, v = synth.make_qkv(2, 16, 8, 8192, 128, base=13, device="cuda")
+    od = attn_fwd(q, k, v, causal=True)
+    torch.cuda.synchronize()
+    qh, kh, vh = (t.cpu().pin_memory() for t in (q, k, v))
+    oh = torch.empty_like(qh).pin_memory()
+    attn_fwd_host(qh, kh, vh, oh, causal=True)
+    assert attn_last_launch_info()["kernel_launches"] > 1
+    assert torch.equal(od.cpu().view(torch.int16), oh.view(torch.int16))
