@@ -67,9 +67,15 @@ typedef enum {
   ATTN_MAP_SWIZZLED_BLOCK_FIRST = 3 /* PAPER.md:236-243, SPEC.md:172 */
 } attn_mapping_t;
 
+/* OR into `mapping`: visit the work units of every (b, h) in DESCENDING
+ * order (longest causal unit first) instead of the paper's ascending order
+ * (PAPER.md:226, :246).  Applied identically under every mapping; it changes
+ * only the schedule, never the result bits. */
+#define ATTN_ORDER_DESCENDING 0x100
+
 typedef enum {
   ATTN_OK = 0,
-  ATTN_ERR_INVALID_VALUE = 1, /* null pointer, size <= 0, Hq % Hkv != 0, mapping not in 0..3,
+  ATTN_ERR_INVALID_VALUE = 1, /* null pointer, size <= 0, Hq % Hkv != 0, bad mapping value,
                                  non-finite scale, overlap, not device memory */
   ATTN_ERR_UNSUPPORTED = 2,   /* d > 128 or d % 8 != 0; N % 128 != 0; misaligned; scale < 0;
                                  device is not sm_100 */

@@ -198,6 +198,12 @@ def build_queues(mapping: str, B: int, Hq: int, Hkv: int, nblk: int,
     return [tiles[cuts[d]:cuts[d + 1]] for d in range(D)]
 
 
+def descending(queues: List[List[Tile]], nblk: int) -> List[List[Tile]]:
+    """The same queues with every (b, h)'s blocks visited last-first (DESIGN.md
+    R19: an order knob applied identically under every mapping)."""
+    return [[(b, h, nblk - 1 - k) for (b, h, k) in q] for q in queues]
+
+
 def is_bijection(queues: List[List[Tile]], B: int, Hq: int, nblk: int) -> bool:
     """every tile appears exactly once across the queues."""
     flat = [t for q in queues for t in q]

@@ -33,10 +33,16 @@ def _check(rc: int) -> None:
         raise AttnError(rc, _lib.load().attn_last_error().decode())
 
 
-def _mapping_id(mapping) -> int:
-    if isinstance(mapping, int):
-        return mapping
-    return MAPPINGS[str(mapping).lower()]
+ORDER_DESCENDING = 0x100  # include/attn_numa.h ATTN_ORDER_DESCENDING
+
+
+def _mapping_id(mapping, order: str = "ascending") -> int:
+    m = mapping if isinstance(mapping, int) else MAPPINGS[str(mapping).lower()]
+    if order == "descending":
+        m |= ORDER_DESCENDING
+    elif order != "ascending":
+        raise ValueError("order must be 'ascending' or 'descending'")
+    return m
 
 
 def _stream_ptr(stream: Optional[torch.cuda.Stream]) -> int:
@@ -46,12 +52,14 @@ def _stream_ptr(stream: Optional[torch.cuda.Stream]) -> int:
 
 def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: Optional[torch.Tensor] = None, *,
              causal: bool = False, scale: Optional[float] = None, mapping="swizzled_head_first",
-             stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+             order: str = "ascending", stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
     """O = softmax(scale * Q K^T) V (PAPER.md eq:fa) on bf16 [B, H, N, d] CUDA tensors.
 
     q: [B, Hq, N, d]; k, v: [B, Hkv, N, d]; returns o [B, Hq, N, d] (allocated
     if not given).  scale defaults to 1/sqrt(d).  Asynchronous on `stream`
-    (default: torch's current stream).
+    (default: torch's current stream).  `order` = "descending" visits each
+    head's work units longest-first (ATTN_ORDER_DESCENDING); results are
+    bit-identical either way.
     """
     for name, t in (("q", q), ("k", k), ("v", v)):
         if not isinstance(t, torch.Tensor) or t.dtype != torch.bfloat16 or not t.is_cuda:
@@ -70,12 +78,12 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: Optional[torc
         scale = 1.0 / math.sqrt(d)
     lib = _lib.load()
     _check(lib.attn_fwd_stream(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), B, Hq, Hkv, N, d,
-                               int(bool(causal)), float(scale), _mapping_id(mapping), _stream_ptr(stream)))
+                               int(bool(causal)), float(scale), _mapping_id(mapping, order), _stream_ptr(stream)))
     return o
 
 
 def attn_fwd_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor, *, causal: bool = False,
-                  scale: Optional[float] = None, mapping="swizzled_head_first",
+                  scale: Optional[float] = None, mapping="swizzled_head_first", order: str = "ascending",
                   stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
     """End-to-end call on HOST (ideally pinned) bf16 tensors: H2D, kernel, D2H, sync."""
     for t in (q, k, v, o):
@@ -87,7 +95,7 @@ def attn_fwd_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Te
         scale = 1.0 / math.sqrt(d)
     lib = _lib.load()
     _check(lib.attn_fwd_host(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), B, Hq, Hkv, N, d,
-                             int(bool(causal)), float(scale), _mapping_id(mapping), _stream_ptr(stream)))
+                             int(bool(causal)), float(scale), _mapping_id(mapping, order), _stream_ptr(stream)))
     return o
 
 
@@ -143,8 +151,8 @@ def decode_trace(buf: torch.Tensor) -> torch.Tensor:
     return buf.view(-1, rec_words)[:, :8].cpu()
 
 
-def attn_schedule_order(B: int, Hq: int, Hkv: int, N: int, mapping, sms_per_domain: Sequence[int]
-                        ) -> List[List[tuple]]:
+def attn_schedule_order(B: int, Hq: int, Hkv: int, N: int, mapping, sms_per_domain: Sequence[int],
+                        order: str = "ascending") -> List[List[tuple]]:
     """Host-side queues (lists of (b, h, unit)) the kernel would pop (unit = 256 rows)."""
     lib = _lib.load()
     U = (N + 255) // 256
@@ -153,7 +161,7 @@ def attn_schedule_order(B: int, Hq: int, Hkv: int, N: int, mapping, sms_per_doma
     nq = ctypes.c_int(0)
     qlen = (ctypes.c_int * _lib.ATTN_MAX_DOMAINS)()
     sizes = (ctypes.c_int * len(sms_per_domain))(*sms_per_domain)
-    _check(lib.attn_schedule_order(B, Hq, Hkv, N, _mapping_id(mapping), len(sms_per_domain),
+    _check(lib.attn_schedule_order(B, Hq, Hkv, N, _mapping_id(mapping, order), len(sms_per_domain),
                                    ctypes.cast(sizes, ctypes.c_void_p), ctypes.cast(out, ctypes.c_void_p), cap,
                                    ctypes.cast(ctypes.pointer(nq), ctypes.c_void_p),
                                    ctypes.cast(qlen, ctypes.c_void_p)))

@@ -340,7 +340,8 @@ int validate(const void* q, const void* k, const void* v, void* o, int B, int Hq
   if (!q || !k || !v || !o) return fail(ATTN_ERR_INVALID_VALUE, "null pointer");
   if (B <= 0 || Hq <= 0 || Hkv <= 0 || N <= 0 || d <= 0) return fail(ATTN_ERR_INVALID_VALUE, "size <= 0");
   if (Hq % Hkv != 0) return fail(ATTN_ERR_INVALID_VALUE, "Hq % Hkv != 0 (non-uniform GQA groups)");
-  if (mapping < 0 || mapping > 3) return fail(ATTN_ERR_INVALID_VALUE, "mapping not in {0,1,2,3}");
+  if ((mapping & ~(kMapMask | kOrderDescending)) || (mapping & kMapMask) > 3)
+    return fail(ATTN_ERR_INVALID_VALUE, "mapping not in {0,1,2,3} (| ATTN_ORDER_DESCENDING)");
   if (!std::isfinite(scale)) return fail(ATTN_ERR_INVALID_VALUE, "non-finite scale");
   const size_t qb = (size_t)B * Hq * N * d * 2, kb = (size_t)B * Hkv * N * d * 2;
   if (overlaps(o, qb, q, qb) || overlaps(o, qb, k, kb) || overlaps(o, qb, v, kb))
@@ -619,6 +620,7 @@ int attn_schedule_order(int B, int Hq, int Hkv, int N, int mapping, int n_domain
     for (int pos = 0; pos < sp.q[qi].len; ++pos) {
       int b, h, u;
       decode_unit(sp.q[qi], pos, Hq, U, b, h, u);
+      if (sp.descending) u = U - 1 - u;
       out[3 * w] = b;
       out[3 * w + 1] = h;
       out[3 * w + 2] = u;

@@ -427,6 +427,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int pos = atomicAdd(&p.counters[qq * 32], 1);
           if (pos < p.sched.q[qq].len) {
             decode_unit(p.sched.q[qq], pos, p.Hq, p.U, b, h, u);
+            if (p.sched.descending) u = p.U - 1 - u;
             qi = qq;
             stolen = t > 0;
             break;

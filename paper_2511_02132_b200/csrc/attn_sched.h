@@ -46,6 +46,7 @@ struct QueueDesc {
 struct SchedParams {
   int n_queues;
   int steal;                           // pop other queues when the own one is empty
+  int descending;                      // units of a head in descending order (longest causal unit first)
   int queue_of_domain[kMaxQueues];     // die -> queue popped first
   QueueDesc q[kMaxQueues];
 };
@@ -87,11 +88,19 @@ inline int prop_cut(long long total, const int* sizes, int n, int d) {
   return (int)((total * acc + S / 2) / S);
 }
 
-// Build the queues of `mapping` (0 BF, 1 HF, 2 SHF, 3 SBF) for n_domains dies.
-// Returns false on bad arguments.
-inline bool build_sched(int mapping, int B, int Hq, int Hkv, int U, int n_domains, const int* sms_per_domain,
+// Mapping argument: low byte = mapping (0 BF, 1 HF, 2 SHF, 3 SBF); bit 8 =
+// descending unit order inside every (b, h) (applied identically to every
+// mapping; the paper's order is ascending).
+constexpr int kMapMask = 0xff;
+constexpr int kOrderDescending = 0x100;
+
+// Build the queues of `mapping` for n_domains dies.  Returns false on bad arguments.
+inline bool build_sched(int mapping_arg, int B, int Hq, int Hkv, int U, int n_domains, const int* sms_per_domain,
                         SchedParams& sp) {
   sp = SchedParams{};
+  if (mapping_arg & ~(kMapMask | kOrderDescending)) return false;
+  const int mapping = mapping_arg & kMapMask;
+  sp.descending = (mapping_arg & kOrderDescending) ? 1 : 0;
   if (B <= 0 || Hq <= 0 || Hkv <= 0 || U <= 0 || Hq % Hkv != 0) return false;
   if (n_domains < 1 || n_domains > kMaxQueues) return false;
   const int G = Hq / Hkv;

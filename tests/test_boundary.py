@@ -48,7 +48,7 @@ def _fwd(lib, q=1 << 20, k=2 << 20, v=3 << 20, o=4 << 20, B=1, Hq=2, Hkv=2, N=12
 
 @pytest.mark.parametrize("kw,status", [
     (dict(q=0), 1), (dict(o=0), 1), (dict(B=0), 1), (dict(N=-1), 1), (dict(Hq=6, Hkv=4), 1),
-    (dict(mapping=4), 1), (dict(mapping=-1), 1), (dict(scale=float("nan")), 1), (dict(scale=float("inf")), 1),
+    (dict(mapping=4), 1), (dict(mapping=-1), 1), (dict(mapping=0x200), 1), (dict(mapping=0x104), 1), (dict(scale=float("nan")), 1), (dict(scale=float("inf")), 1),
     (dict(d=100), 2), (dict(d=136), 2), (dict(N=200), 2), (dict(scale=-0.5), 2), (dict(q=(1 << 20) + 8), 2),
     (dict(o=(1 << 20) + 64), 1),   # o overlaps q
 ])
@@ -83,6 +83,18 @@ def test_schedule_order_matches_oracle(lib, mapping):
         got = api.attn_schedule_order(B, Hq, Hkv, N, mapping, sizes)
         want = om.build_queues(mapping, B, Hq, Hkv, U, sizes)
         assert got == want, (mapping, B, Hq, Hkv, N, sizes)
+
+
+def test_schedule_order_descending_matches_oracle(lib):
+    rng = random.Random(11)
+    for _ in range(30):
+        Hkv = rng.choice([1, 2, 4, 8])
+        Hq = Hkv * rng.choice([1, 2])
+        B, N = rng.randint(1, 2), 128 * rng.randint(1, 10)
+        U = (N + 255) // 256
+        for m in om.MAPPINGS:
+            got = api.attn_schedule_order(B, Hq, Hkv, N, m, [74, 74], order="descending")
+            assert got == om.descending(om.build_queues(m, B, Hq, Hkv, U, [74, 74]), U)
 
 
 def test_schedule_order_baseline_configs(lib):
