@@ -30,6 +30,8 @@
  *    all bf16 (raw 16-bit storage, passed as void*).  Accumulation is fp32.
  *  - GQA grouping: query head h reads K/V head h / (Hq / Hkv).
  *  - causal != 0 masks key j from query i when j > i (N_q == N_k).
+ *  - Any N >= 1: a ragged last block is handled with TMA out-of-bounds
+ *    zero fill, key masking and row-guarded stores.
  *  - Head dim d: any multiple of 8 up to 128 (DeepSeek-V3's 56, PAPER.md:417,
  *    included).  The kernel runs at 64 or 128 columns; TMA zero-fills the
  *    padding columns on load and they are never stored.
@@ -77,7 +79,7 @@ typedef enum {
   ATTN_OK = 0,
   ATTN_ERR_INVALID_VALUE = 1, /* null pointer, size <= 0, Hq % Hkv != 0, bad mapping value,
                                  non-finite scale, overlap, not device memory */
-  ATTN_ERR_UNSUPPORTED = 2,   /* d > 128 or d % 8 != 0; N % 128 != 0; misaligned; scale < 0;
+  ATTN_ERR_UNSUPPORTED = 2,   /* d > 128 or d % 8 != 0; misaligned; scale < 0;
                                  device is not sm_100 */
   ATTN_ERR_CUDA = 3,          /* CUDA runtime / driver failure (see attn_last_error) */
   ATTN_ERR_TOPOLOGY = 4       /* the die probe itself failed (an inconclusive probe is

@@ -347,7 +347,6 @@ int validate(const void* q, const void* k, const void* v, void* o, int B, int Hq
   if (overlaps(o, qb, q, qb) || overlaps(o, qb, k, kb) || overlaps(o, qb, v, kb))
     return fail(ATTN_ERR_INVALID_VALUE, "o overlaps an input");
   if (d > 128 || d % 8 != 0) return fail(ATTN_ERR_UNSUPPORTED, "head dim must be a multiple of 8 and <= 128");
-  if (N % 128 != 0) return fail(ATTN_ERR_UNSUPPORTED, "N must be a multiple of 128");
   if (scale < 0.f) return fail(ATTN_ERR_UNSUPPORTED, "negative scale");
   if ((long long)B * Hq * N >= (1ll << 31) || (long long)B * Hkv * N >= (1ll << 31))
     return fail(ATTN_ERR_UNSUPPORTED, "B*H*N exceeds 2^31 rows");
@@ -356,12 +355,26 @@ int validate(const void* q, const void* k, const void* v, void* o, int B, int Hq
   return ATTN_OK;
 }
 
-int make_tmap(CUtensorMap* m, const void* base, long long rows, int d) {
-  cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)d * 2};
-  cuuint32_t box[2] = {64, 128};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+// 3-D view [heads][N][d] of a [B][H][N][d] tensor: a box never crosses into
+// the next head, and rows >= N are out of bounds (zero-filled by TMA).
+int make_tmap(CUtensorMap* m, const void* base, long long heads, int N, int d, int box_rows) {
+#ifdef ATTN_TMA_2D
+  {
+    cuuint64_t dims2[2] = {(cuuint64_t)d, (cuuint64_t)N * heads};
+    cuuint64_t strides2[1] = {(cuuint64_t)d * 2};
+    cuuint32_t box2[2] = {64, (cuuint32_t)box_rows};
+    cuuint32_t estr2[2] = {1, 1};
+    CUresult r2 = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims2, strides2, box2,
+                           estr2, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r2 == CUDA_SUCCESS ? ATTN_OK : fail(ATTN_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  }
+#endif
+  cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)N, (cuuint64_t)heads};
+  cuuint64_t strides[2] = {(cuuint64_t)d * 2, (cuuint64_t)N * d * 2};
+  cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(ATTN_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
@@ -404,7 +417,7 @@ int fwd_impl(const void* q, const void* k, const void* v, void* o, int B, int Hq
   rc = ensure_init(dev, st);
   if (rc != ATTN_OK) return rc;
 
-  const int nblk = N / kBlockM;
+  const int nblk = (N + kBlockM - 1) / kBlockM;  // last block may be ragged
   const int U = (nblk + 1) / 2;
   KernelParams kp{};
   kp.B = B; kp.Hq = Hq; kp.Hkv = Hkv; kp.N = N; kp.G = Hq / Hkv; kp.U = U; kp.nblk = nblk;
@@ -422,9 +435,9 @@ int fwd_impl(const void* q, const void* k, const void* v, void* o, int B, int Hq
   kp.trace_cap = st.trace_cap;
 
   CUtensorMap tq, tk, tv;
-  if ((rc = make_tmap(&tq, q, (long long)B * Hq * N, d)) != ATTN_OK) return rc;
-  if ((rc = make_tmap(&tk, k, (long long)B * Hkv * N, d)) != ATTN_OK) return rc;
-  if ((rc = make_tmap(&tv, v, (long long)B * Hkv * N, d)) != ATTN_OK) return rc;
+  if ((rc = make_tmap(&tq, q, (long long)B * Hq, N, d, kBlockM)) != ATTN_OK) return rc;
+  if ((rc = make_tmap(&tk, k, (long long)B * Hkv, N, d, kBlockN)) != ATTN_OK) return rc;
+  if ((rc = make_tmap(&tv, v, (long long)B * Hkv, N, d, kBlockN)) != ATTN_OK) return rc;
 
   const int total = B * Hq * U;
   const int grid = std::min(st.num_sms, total);

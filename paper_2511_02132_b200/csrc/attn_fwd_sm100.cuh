@@ -27,6 +27,7 @@
 #include <cuda_bf16.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "../../include/attn_numa.h"
 #include "attn_sched.h"
@@ -228,18 +229,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int ntile = n1 > 0 ? 2 : 1;
         ptx::mbar_arrive_expect_tx(&ctrl->q_full, ntile * C::kQTileBytes);
         for (int t = 0; t < ntile; ++t) {
-          const int row = (b * p.Hq + h) * p.N + (2 * u + t) * kBlockM;
+          // 3-D view [B*Hq][N][d]: rows >= N of this head are out of bounds (zero-filled)
+          const int bh = b * p.Hq + h, row = (2 * u + t) * kBlockM;
 #pragma unroll
           for (int c = 0; c < C::kChunks; ++c)
-            ptx::tma_load_2d(q_smem + t * C::kQTileBytes + c * kBlockM * 128, &tm_q, &ctrl->q_full, c * 64, row,
+#ifdef ATTN_TMA_2D
+            ptx::tma_load_2d(q_smem + t * C::kQTileBytes + c * kBlockM * 128, &tm_q, &ctrl->q_full, c * 64,
+                             bh * p.N + row, pol_q);
+#else
+            ptx::tma_load_3d(q_smem + t * C::kQTileBytes + c * kBlockM * 128, &tm_q, &ctrl->q_full, c * 64, row, bh,
                              pol_q);
+#endif
         }
-        const int kvrow = (b * p.Hkv + h / p.G) * p.N;
+        const int kvbh = b * p.Hkv + h / p.G;
         for (int j = 0; j < n; ++j) {
 #pragma unroll
           for (int which = 0; which < 2; ++which) {
             ptx::mbar_wait(&ctrl->kv_empty[kv_stage], kv_phase ^ 1);
-      #ifdef ATTN_DEBUG_NO_KV_LOAD
+#ifdef ATTN_DEBUG_NO_KV_LOAD
             if (j >= 2) {  // bandwidth probe: reuse whatever is in the slot
               ptx::mbar_arrive(&ctrl->kv_full[kv_stage]);
               if (++kv_stage == C::kStages) { kv_stage = 0; kv_phase ^= 1; }
@@ -250,8 +257,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint8_t* dst = kv_smem + kv_stage * C::kKVBytes;
 #pragma unroll
             for (int c = 0; c < C::kChunks; ++c)
+#ifdef ATTN_TMA_2D
               ptx::tma_load_2d(dst + c * kBlockN * 128, which == 0 ? (const void*)&tm_k : (const void*)&tm_v,
-                               &ctrl->kv_full[kv_stage], c * 64, kvrow + j * kBlockN, pol_kv);
+                               &ctrl->kv_full[kv_stage], c * 64, kvbh * p.N + j * kBlockN, pol_kv);
+#else
+              ptx::tma_load_3d(dst + c * kBlockN * 128, which == 0 ? (const void*)&tm_k : (const void*)&tm_v,
+                               &ctrl->kv_full[kv_stage], c * 64, j * kBlockN, kvbh, pol_kv);
+#endif
             if (++kv_stage == C::kStages) { kv_stage = 0; kv_phase ^= 1; }
           }
         }
@@ -494,7 +506,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int nt = (t == 0) ? n0 : n1;
       if (nt == 0) continue;
       const int qb = 2 * e.z + t;
-      const int lim = row - cbase;  // diagonal block: local key k visible iff k <= lim
+      // keys of the last key block that exist (ragged N): local key k < tail_keys
+      const int last_blk = p.nblk - 1;
+      const int tail_lim = (p.N - last_blk * kBlockN - 1) - cbase;  // last block: local k visible iff k <= tail_lim
 #ifdef ATTN_TIMELINE
       const bool first_unit = (gblk == 0);
 #endif
@@ -517,8 +531,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t r[kCols];
         if constexpr (kCols == 128) ptx::tmem_ld128(trow + colS, r);
         else ptx::tmem_ld64(trow + colS, r);
-        const bool diag = kCausal && (j == qb);
-        if (diag) {  // causal mask on the diagonal block: key > row -> -inf
+        // visible local keys are k <= lim: causal diagonal block (key <= query)
+        // and/or the ragged last key block (key < N)
+        int lim = kCols;
+        if (kCausal && j == qb) lim = row - cbase;
+        if (j == last_blk && tail_lim < lim) lim = tail_lim;
+        // warp-uniform choice between the masked and the unmasked loop bodies
+        const bool diag = __any_sync(0xffffffffu, lim < kCols - 1);
+        if (diag) {  // masked keys -> -inf
 #pragma unroll
           for (int k = 0; k < kCols; ++k)
             if (k > lim) r[k] = 0xff800000u;
@@ -569,6 +589,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // core starts O += P V on the first half while the second is computed.
         float2 sq[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                         make_float2(0.f, 0.f)};
+        auto exp_block = [&](auto mask_tag) {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
 #pragma unroll
@@ -585,7 +606,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               pr.y = ptx::ex2(x.y);
 #endif
             }
-            if (diag) {
+            if constexpr (decltype(mask_tag)::value) {
               pr.x = (k <= lim) ? pr.x : 0.f;
               pr.y = (k + 1 <= lim) ? pr.y : 0.f;
             }
@@ -602,6 +623,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (tls) tls[1 + h] = clock64();
 #endif
         }
+        };
+        if (diag) exp_block(std::true_type{});
+        else exp_block(std::false_type{});
         const float2 s01 = ptx::fadd2(sq[0], sq[1]), s23 = ptx::fadd2(sq[2], sq[3]);
         const float2 s4 = ptx::fadd2(s01, s23);
         const float sum = s4.x + s4.y;
@@ -620,7 +644,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float inv_l = 1.f / l;
       const long long orow = ((long long)(e.x * p.Hq + e.y) * p.N + (long long)qb * kBlockM + row) * p.d_real;
       uint4* dst = reinterpret_cast<uint4*>(p.o + orow + hf * kOCols);
-      const int ncol = p.d_real - hf * kOCols;  // real columns of this thread's slice (multiple of 8)
+      // real columns of this thread's slice (multiple of 8); rows >= N (ragged
+      // last query block) store nothing but still join the warp-wide TMEM loads
+      const int ncol = (qb * kBlockM + row < p.N) ? p.d_real - hf * kOCols : 0;
 #pragma unroll
       for (int cc = 0; cc < kOCols; cc += 32) {
         uint32_t o[32];

@@ -53,6 +53,11 @@ SMALL = [
     (2, 4, 2, 384, 96, False),    # padded to 128
     (1, 2, 2, 256, 8, True),      # smallest head dim
     (1, 2, 1, 640, 120, True),
+    (1, 2, 2, 200, 128, False),   # ragged N: one full and one 72-row block
+    (2, 4, 2, 1000, 64, True),    # ragged N, causal, GQA
+    (1, 3, 3, 77, 56, True),      # N smaller than one block, padded head dim
+    (1, 2, 2, 1, 128, False),     # a single token
+    (1, 4, 4, 300, 128, False),   # 3 blocks, last unit half empty and ragged
 ]
 
 
