@@ -44,6 +44,8 @@ def _load():
         lib.oracle_attn_weights.argtypes = common + [i64, i64, i64, vp, vp]
         for f in (lib.oracle_attn_full, lib.oracle_attn_rows, lib.oracle_attn_weights):
             f.restype = i32
+        lib.oracle_attn_bwd.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, f64, vp, vp, vp, vp]
+        lib.oracle_attn_bwd.restype = i32
         lib.oracle_set_threads.argtypes = [i32]
         lib.oracle_set_threads.restype = None
         lib.oracle_max_threads.argtypes = []
@@ -141,3 +143,25 @@ def attention_weights(q, k, v, b: int, h: int, i: int, causal: bool = False,
     if rc != 0:
         raise ValueError(f"oracle_attn_weights failed ({rc})")
     return w, o
+
+
+def attention_bwd(q, k, v, dout, causal: bool = False, scale: float | None = None):
+    """fp64 gradients (dq, dk, dv) of sum(dout * attention(q, k, v)) and the
+    natural-log row LSE, per eq:ba.  O(N^2) memory per head:
+    small shapes only."""
+    qa, ka, va, code, (B, Hq, Hkv, N, d) = _prep(q, k, v)
+    da, cd = _as_np(dout)
+    if cd != code or da.shape != qa.shape:
+        raise ValueError("dout must match q in shape and element type")
+    if scale is None:
+        scale = 1.0 / float(np.sqrt(d))
+    dq = np.empty((B, Hq, N, d), dtype=np.float64)
+    dk = np.empty((B, Hkv, N, d), dtype=np.float64)
+    dv = np.empty((B, Hkv, N, d), dtype=np.float64)
+    lse = np.empty((B, Hq, N), dtype=np.float64)
+    rc = _load().oracle_attn_bwd(qa.ctypes.data, ka.ctypes.data, va.ctypes.data, da.ctypes.data, code, B, Hq, Hkv, N,
+                                 d, int(bool(causal)), float(scale), dq.ctypes.data, dk.ctypes.data, dv.ctypes.data,
+                                 lse.ctypes.data)
+    if rc != 0:
+        raise ValueError(f"oracle_attn_bwd failed ({rc})")
+    return dq, dk, dv, lse

@@ -181,3 +181,84 @@ int oracle_attn_weights(const void *q, const void *k, const void *v, int dtype,
     free(s);
     return 0;
 }
+
+/* ------------------------------------------------------------------ backward
+ * PAPER.md:157-165 (eq:ba), for P = softmax(scale * Q K^T) (masked as in the
+ * forward) and an upstream gradient dO:
+ *   dV = P^T dO,   dP = dO V^T,   dS = dsoftmax(dP) = P o (dP - rowsum(P o dP)),
+ *   dQ = scale * dS K,   dK = scale * dS^T Q.
+ * GQA: dK, dV of a KV group sum over the query heads of the group.
+ * Plain definition: per (b, h) the full N x N matrices P and dP in fp64; no
+ * tiling, no recomputation tricks.  Outputs are fp64, zero-initialised here.
+ * Also returns lse[b,h,i] = log sum_j exp(scale * s_ij) (natural log) when lse
+ * is non-NULL. */
+int oracle_attn_bwd(const void *q, const void *k, const void *v, const void *dout, int dtype,
+                    int B, int Hq, int Hkv, int N, int d, int causal, double scale,
+                    double *dq, double *dk, double *dv, double *lse) {
+    if (oracle_check(dtype, B, Hq, Hkv, N, d)) return 1;
+    const int G = Hq / Hkv;
+    const int64_t hsz = (int64_t)N * d;
+    for (int64_t x = 0; x < (int64_t)B * Hq * hsz; ++x) dq[x] = 0.0;
+    for (int64_t x = 0; x < (int64_t)B * Hkv * hsz; ++x) { dk[x] = 0.0; dv[x] = 0.0; }
+    double *P = (double *)malloc(sizeof(double) * (size_t)N * N);
+    double *dP = (double *)malloc(sizeof(double) * (size_t)N * N);
+    if (!P || !dP) { free(P); free(dP); return 2; }
+    for (int b = 0; b < B; ++b) {
+        for (int h = 0; h < Hq; ++h) {
+            const int g = h / G;
+            const int64_t qo = ((int64_t)b * Hq + h) * hsz, ko = ((int64_t)b * Hkv + g) * hsz;
+            /* P: row-wise two-pass softmax (same definition as the forward) */
+#pragma omp parallel for schedule(dynamic, 8)
+            for (int i = 0; i < N; ++i) {
+                const int nvis = causal ? i + 1 : N;
+                double m = -INFINITY;
+                for (int j = 0; j < nvis; ++j) {
+                    double acc = 0.0;
+                    for (int c = 0; c < d; ++c)
+                        acc += oracle_widen(q, dtype, qo + (int64_t)i * d + c) *
+                               oracle_widen(k, dtype, ko + (int64_t)j * d + c);
+                    P[(int64_t)i * N + j] = scale * acc;
+                    if (P[(int64_t)i * N + j] > m) m = P[(int64_t)i * N + j];
+                }
+                double l = 0.0;
+                for (int j = 0; j < nvis; ++j) {
+                    P[(int64_t)i * N + j] = exp(P[(int64_t)i * N + j] - m);
+                    l += P[(int64_t)i * N + j];
+                }
+                for (int j = 0; j < N; ++j) P[(int64_t)i * N + j] = (j < nvis) ? P[(int64_t)i * N + j] / l : 0.0;
+                if (lse) lse[((int64_t)b * Hq + h) * N + i] = m + log(l);
+                /* dP = dO V^T, then dS = P o (dP - rowsum(P o dP)) in place */
+                double dot = 0.0;
+                for (int j = 0; j < N; ++j) {
+                    double acc = 0.0;
+                    if (j < nvis)
+                        for (int c = 0; c < d; ++c)
+                            acc += oracle_widen(dout, dtype, qo + (int64_t)i * d + c) *
+                                   oracle_widen(v, dtype, ko + (int64_t)j * d + c);
+                    dP[(int64_t)i * N + j] = acc;
+                    dot += P[(int64_t)i * N + j] * acc;
+                }
+                for (int j = 0; j < N; ++j) dP[(int64_t)i * N + j] = P[(int64_t)i * N + j] * (dP[(int64_t)i * N + j] - dot);
+                /* dQ_i = scale * sum_j dS_ij K_j */
+                for (int j = 0; j < nvis; ++j)
+                    for (int c = 0; c < d; ++c)
+                        dq[qo + (int64_t)i * d + c] += scale * dP[(int64_t)i * N + j] * oracle_widen(k, dtype, ko + (int64_t)j * d + c);
+            }
+            /* dV_j += sum_i P_ij dO_i ;  dK_j += scale * sum_i dS_ij Q_i */
+#pragma omp parallel for schedule(dynamic, 8)
+            for (int j = 0; j < N; ++j) {
+                for (int i = 0; i < N; ++i) {
+                    const double p = P[(int64_t)i * N + j], ds = dP[(int64_t)i * N + j];
+                    if (p == 0.0 && ds == 0.0) continue;
+                    for (int c = 0; c < d; ++c) {
+                        dv[ko + (int64_t)j * d + c] += p * oracle_widen(dout, dtype, qo + (int64_t)i * d + c);
+                        dk[ko + (int64_t)j * d + c] += scale * ds * oracle_widen(q, dtype, qo + (int64_t)i * d + c);
+                    }
+                }
+            }
+        }
+    }
+    free(P);
+    free(dP);
+    return 0;
+}
