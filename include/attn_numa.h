@@ -127,6 +127,27 @@ ATTN_API int attn_fwd(const void* q, const void* k, const void* v, void* o, int 
 ATTN_API int attn_fwd_stream(const void* q, const void* k, const void* v, void* o, int B, int Hq, int Hkv, int N,
                     int d, int causal, float scale, int mapping, void* cuda_stream);
 
+/* Same as attn_fwd_stream and also writes lse[B][Hq][N] (fp32, device
+ * memory): lse[b,h,i] = log sum_j exp(scale * s_ij) over the visible keys
+ * (natural log), the per-row statistic the backward pass needs. */
+ATTN_API int attn_fwd_lse(const void* q, const void* k, const void* v, void* o, float* lse, int B, int Hq, int Hkv,
+                          int N, int d, int causal, float scale, int mapping, void* cuda_stream);
+
+/* Backward pass (eq:ba) on the stream `cuda_stream`:
+ *   dV = P^T dO,  dP = dO V^T,  dS = P o (dP - rowsum(dO o O)),
+ *   dQ = scale * dS K,  dK = scale * dS^T Q,   P = exp(scale * Q K^T - lse).
+ * q, k, v, o, dout: device bf16 in the forward's layouts; lse: device fp32
+ * [B][Hq][N] from attn_fwd_lse; dq [B][Hq][N][d], dk, dv [B][Hkv][N][d]: device
+ * bf16 outputs, fully written (GQA: dk, dv sum over the group's query heads).
+ * `mapping` orders the work units exactly as for the forward (dQ: query
+ * blocks of a head; dK/dV: key blocks of a KV group).  Three launches:
+ * rowsum(dO o O) into library workspace, the dQ kernel, the dK/dV kernel.
+ * Same validation and status codes as attn_fwd; gradients must not overlap
+ * each other or any input. */
+ATTN_API int attn_bwd(const void* q, const void* k, const void* v, const void* o, const void* dout,
+                      const float* lse, void* dq, void* dk, void* dv, int B, int Hq, int Hkv, int N, int d,
+                      int causal, float scale, int mapping, void* cuda_stream);
+
 /* End-to-end variant on HOST buffers (same layout): copies q/k/v host->device
  * into library-owned device buffers, runs the kernel, copies o device->host
  * and synchronises `cuda_stream` before returning.  Large problems are split

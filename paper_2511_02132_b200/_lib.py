@@ -16,7 +16,7 @@ ATTN_MAX_SMID = 512
 
 # every symbol include/attn_numa.h declares (checked by tests/test_boundary.py)
 EXPORTS = (
-    "attn_fwd", "attn_fwd_stream", "attn_fwd_host", "attn_set_stream", "attn_init", "attn_topology",
+    "attn_fwd", "attn_fwd_stream", "attn_fwd_lse", "attn_bwd", "attn_fwd_host", "attn_set_stream", "attn_init", "attn_topology",
     "attn_set_topology_override", "attn_set_schedule_trace", "attn_schedule_order",
     "attn_last_launch_info", "attn_status_string", "attn_last_error", "attn_version", "attn_shutdown",
 )
@@ -69,6 +69,8 @@ def load():
     lib.attn_fwd.argtypes = fwd_args
     lib.attn_fwd_stream.argtypes = fwd_args + [vp]
     lib.attn_fwd_host.argtypes = fwd_args + [vp]
+    lib.attn_fwd_lse.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, i32, i32, i32, f32, i32, vp]
+    lib.attn_bwd.argtypes = [vp] * 9 + [i32, i32, i32, i32, i32, i32, f32, i32, vp]
     lib.attn_set_stream.argtypes = [vp]
     lib.attn_init.argtypes = [i32]
     lib.attn_topology.argtypes = [i32, ctypes.POINTER(Topology)]
@@ -76,7 +78,7 @@ def load():
     lib.attn_set_schedule_trace.argtypes = [i32, vp, ll]
     lib.attn_schedule_order.argtypes = [i32, i32, i32, i32, i32, i32, vp, vp, ll, vp, vp]
     lib.attn_last_launch_info.argtypes = [ctypes.POINTER(LaunchInfo)]
-    for f in ("attn_fwd", "attn_fwd_stream", "attn_fwd_host", "attn_set_stream", "attn_init", "attn_topology",
+    for f in ("attn_fwd", "attn_fwd_stream", "attn_fwd_lse", "attn_bwd", "attn_fwd_host", "attn_set_stream", "attn_init", "attn_topology",
               "attn_set_topology_override", "attn_set_schedule_trace", "attn_schedule_order",
               "attn_last_launch_info"):
         getattr(lib, f).restype = i32

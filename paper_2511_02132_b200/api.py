@@ -82,6 +82,42 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: Optional[torc
     return o
 
 
+def attn_fwd_lse(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool = False,
+                 scale: Optional[float] = None, mapping="swizzled_head_first", order: str = "ascending",
+                 stream: Optional[torch.cuda.Stream] = None):
+    """Forward that also returns the fp32 row log-sum-exp [B, Hq, N] (backward input)."""
+    B, Hq, N, d = q.shape
+    o = torch.empty_like(q)
+    lse = torch.empty((B, Hq, N), dtype=torch.float32, device=q.device)
+    if scale is None:
+        scale = 1.0 / math.sqrt(d)
+    lib = _lib.load()
+    _check(lib.attn_fwd_lse(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), lse.data_ptr(), B, Hq,
+                            k.shape[1], N, d, int(bool(causal)), float(scale), _mapping_id(mapping, order),
+                            _stream_ptr(stream)))
+    return o, lse
+
+
+def attn_bwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor, dout: torch.Tensor,
+             lse: torch.Tensor, *, causal: bool = False, scale: Optional[float] = None,
+             mapping="swizzled_head_first", order: str = "ascending", stream: Optional[torch.cuda.Stream] = None):
+    """Gradients (dq, dk, dv) of sum(dout * attention(q, k, v)) (PAPER.md eq:ba), bf16."""
+    for name, t in (("q", q), ("k", k), ("v", v), ("o", o), ("dout", dout)):
+        if t.dtype != torch.bfloat16 or not t.is_cuda or not t.is_contiguous():
+            raise TypeError(f"{name} must be a contiguous bfloat16 CUDA tensor")
+    if lse.dtype != torch.float32 or not lse.is_contiguous():
+        raise TypeError("lse must be a contiguous float32 CUDA tensor")
+    B, Hq, N, d = q.shape
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    if scale is None:
+        scale = 1.0 / math.sqrt(d)
+    lib = _lib.load()
+    _check(lib.attn_bwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), dout.data_ptr(), lse.data_ptr(),
+                        dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), B, Hq, k.shape[1], N, d, int(bool(causal)),
+                        float(scale), _mapping_id(mapping, order), _stream_ptr(stream)))
+    return dq, dk, dv
+
+
 def attn_fwd_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor, *, causal: bool = False,
                   scale: Optional[float] = None, mapping="swizzled_head_first", order: str = "ascending",
                   stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:

@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "../../include/attn_numa.h"
+#include "attn_bwd_sm100.cuh"
 #include "attn_fwd_sm100.cuh"
 #include "attn_sched.h"
 #include "topology.cuh"
@@ -62,6 +63,9 @@ struct DevState {
   void* hbuf[4] = {nullptr, nullptr, nullptr, nullptr};
   size_t hbuf_bytes[4] = {0, 0, 0, 0};
   bool e2e_ready = false;
+  float* dvec = nullptr;       // backward workspace: rowsum(dO o O)
+  size_t dvec_elems = 0;
+  bool battr_done[8] = {false, false, false, false, false, false, false, false};
   cudaStream_t e2e_stream[3] = {nullptr, nullptr, nullptr};
   cudaEvent_t e2e_ev[2][kE2EChunks + 1] = {};
 };
@@ -399,7 +403,7 @@ int launch_t(DevState& st, int attr_idx, const CUtensorMap& tq, const CUtensorMa
 }
 
 int fwd_impl(const void* q, const void* k, const void* v, void* o, int B, int Hq, int Hkv, int N, int d, int causal,
-             float scale, int mapping, cudaStream_t stream) {
+             float scale, int mapping, cudaStream_t stream, float* lse = nullptr) {
   int rc = validate(q, k, v, o, B, Hq, Hkv, N, d, scale, mapping);
   if (rc != ATTN_OK) return rc;
   int dev = 0;
@@ -425,6 +429,7 @@ int fwd_impl(const void* q, const void* k, const void* v, void* o, int B, int Hq
   const int dpad = d <= 64 ? 64 : 128;  // kernel head dim; TMA zero-fills columns d..dpad-1
   kp.scale_log2 = scale * 1.4426950408889634f;
   kp.o = reinterpret_cast<__nv_bfloat16*>(o);
+  kp.lse = lse;
   if (!build_sched(mapping, B, Hq, Hkv, U, st.active.n_domains, st.active.sms_per_domain, kp.sched))
     return fail(ATTN_ERR_INVALID_VALUE, "cannot build the schedule");
   const unsigned slot = st.slot++ % kCounterSlots;
@@ -452,6 +457,103 @@ int fwd_impl(const void* q, const void* k, const void* v, void* o, int B, int Hq
   return ATTN_OK;
 }
 
+
+template <int D, bool kCausal>
+int launch_bwd_t(DevState& st, const CUtensorMap& tq, const CUtensorMap& tdo, const CUtensorMap& tk,
+                 const CUtensorMap& tv, bwd::BwdParams pq, bwd::BwdParams pkv, int grid_q, int grid_kv,
+                 cudaStream_t s) {
+  const int idx = (D == 128 ? 0 : 2) + (kCausal ? 1 : 0);
+  auto* kq = bwd::attn_bwd_dq_kernel<D, kCausal>;
+  auto* kkv = bwd::attn_bwd_dkdv_kernel<D, kCausal>;
+  const int smem = bwd::BCfg<D>::kSmemBytes;
+  if (!st.battr_done[idx]) {
+    ATTN_CUDA(cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    ATTN_CUDA(cudaFuncSetAttribute(kkv, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    st.battr_done[idx] = true;
+  }
+  kq<<<grid_q, bwd::kThreads, smem, s>>>(tq, tdo, tk, tv, pq);
+  ATTN_CUDA(cudaGetLastError());
+  kkv<<<grid_kv, bwd::kThreads, smem, s>>>(tq, tdo, tk, tv, pkv);
+  ATTN_CUDA(cudaGetLastError());
+  return ATTN_OK;
+}
+
+int bwd_impl(const void* q, const void* k, const void* v, const void* o, const void* dout, const float* lse, void* dq,
+             void* dk, void* dv, int B, int Hq, int Hkv, int N, int d, int causal, float scale, int mapping,
+             cudaStream_t stream) {
+  int rc = validate(q, k, v, dq, B, Hq, Hkv, N, d, scale, mapping);
+  if (rc != ATTN_OK) return rc;
+  if (!o || !dout || !lse || !dk || !dv) return fail(ATTN_ERR_INVALID_VALUE, "null pointer");
+  const size_t qb = (size_t)B * Hq * N * d * 2, kb = (size_t)B * Hkv * N * d * 2, lb = (size_t)B * Hq * N * 4;
+  for (const void* out : {(const void*)dq, (const void*)dk, (const void*)dv}) {
+    const size_t ob = (out == dq) ? qb : kb;
+    for (auto in : {std::make_pair(q, qb), std::make_pair(k, kb), std::make_pair(v, kb), std::make_pair(o, qb),
+                    std::make_pair(dout, qb), std::make_pair((const void*)lse, lb)})
+      if (overlaps(out, ob, in.first, in.second)) return fail(ATTN_ERR_INVALID_VALUE, "a gradient overlaps an input");
+  }
+  if (overlaps(dq, qb, dk, kb) || overlaps(dq, qb, dv, kb) || overlaps(dk, kb, dv, kb))
+    return fail(ATTN_ERR_INVALID_VALUE, "gradients overlap each other");
+  for (const void* ptr : {o, dout, (const void*)dk, (const void*)dv})
+    if (reinterpret_cast<uintptr_t>(ptr) % 16 != 0) return fail(ATTN_ERR_UNSUPPORTED, "pointer not 16-byte aligned");
+  int dev = 0;
+  if ((rc = current_device(dev)) != ATTN_OK) return rc;
+  for (auto pr : {std::make_pair(q, "q"), std::make_pair(k, "k"), std::make_pair(v, "v"), std::make_pair(o, "o"),
+                  std::make_pair(dout, "dout"), std::make_pair((const void*)lse, "lse"),
+                  std::make_pair((const void*)dq, "dq"), std::make_pair((const void*)dk, "dk"),
+                  std::make_pair((const void*)dv, "dv")})
+    if ((rc = check_dev_ptr(pr.first, dev, pr.second)) != ATTN_OK) return rc;
+  if ((rc = get_encode()) != ATTN_OK) return rc;
+  DevState& st = g_dev[dev];
+  std::lock_guard<std::mutex> lk(st.mu);
+  if ((rc = ensure_init(dev, st)) != ATTN_OK) return rc;
+  const size_t rows = (size_t)B * Hq * N;
+  if (st.dvec_elems < rows) {
+    if (st.dvec) cudaFree(st.dvec);
+    st.dvec = nullptr;
+    st.dvec_elems = 0;
+    ATTN_CUDA(cudaMalloc(&st.dvec, rows * sizeof(float)));
+    st.dvec_elems = rows;
+  }
+  const int nblk = (N + bwd::kBM - 1) / bwd::kBM;
+  bwd::BwdParams pq{};
+  pq.B = B; pq.Hq = Hq; pq.Hkv = Hkv; pq.N = N; pq.G = Hq / Hkv; pq.nblk = nblk; pq.d_real = d;
+  pq.scale = scale; pq.scale_log2 = scale * 1.4426950408889634f;
+  pq.lse = lse; pq.dvec = st.dvec;
+  pq.dq = reinterpret_cast<__nv_bfloat16*>(dq);
+  pq.dk = reinterpret_cast<__nv_bfloat16*>(dk);
+  pq.dv = reinterpret_cast<__nv_bfloat16*>(dv);
+  pq.domain_of_smid = st.d_domain;
+  pq.n_smid = ATTN_MAX_SMID;
+  bwd::BwdParams pkv = pq;
+  // dQ units: (b, query head, query block); dK/dV units: (b, KV group, key block)
+  pq.U = nblk;
+  pkv.U = nblk;
+  if (!build_sched(mapping, B, Hq, Hkv, nblk, st.active.n_domains, st.active.sms_per_domain, pq.sched) ||
+      !build_sched(mapping, B, Hkv, Hkv, nblk, st.active.n_domains, st.active.sms_per_domain, pkv.sched))
+    return fail(ATTN_ERR_INVALID_VALUE, "cannot build the schedule");
+  pq.counters = st.d_counters + (size_t)(st.slot++ % kCounterSlots) * kCounterInts;
+  pkv.counters = st.d_counters + (size_t)(st.slot++ % kCounterSlots) * kCounterInts;
+  CUtensorMap tq, tdo, tk, tv;
+  if ((rc = make_tmap(&tq, q, (long long)B * Hq, N, d, bwd::kBM)) != ATTN_OK) return rc;
+  if ((rc = make_tmap(&tdo, dout, (long long)B * Hq, N, d, bwd::kBM)) != ATTN_OK) return rc;
+  if ((rc = make_tmap(&tk, k, (long long)B * Hkv, N, d, bwd::kBM)) != ATTN_OK) return rc;
+  if ((rc = make_tmap(&tv, v, (long long)B * Hkv, N, d, bwd::kBM)) != ATTN_OK) return rc;
+  const long long nrows = (long long)rows;
+  bwd::attn_bwd_dot_kernel<<<(unsigned)((nrows + 7) / 8), 256, 0, stream>>>(
+      reinterpret_cast<const __nv_bfloat16*>(o), reinterpret_cast<const __nv_bfloat16*>(dout), st.dvec, nrows, d);
+  ATTN_CUDA(cudaGetLastError());
+  const int grid_q = std::min(st.num_sms, B * Hq * nblk), grid_kv = std::min(st.num_sms, B * Hkv * nblk);
+  const int dpad = d <= 64 ? 64 : 128;
+  if (dpad == 128 && causal) rc = launch_bwd_t<128, true>(st, tq, tdo, tk, tv, pq, pkv, grid_q, grid_kv, stream);
+  else if (dpad == 128) rc = launch_bwd_t<128, false>(st, tq, tdo, tk, tv, pq, pkv, grid_q, grid_kv, stream);
+  else if (causal) rc = launch_bwd_t<64, true>(st, tq, tdo, tk, tv, pq, pkv, grid_q, grid_kv, stream);
+  else rc = launch_bwd_t<64, false>(st, tq, tdo, tk, tv, pq, pkv, grid_q, grid_kv, stream);
+  if (rc != ATTN_OK) return rc;
+  g_info.kernel_launches = 3;
+  g_info.units = B * Hq * nblk + B * Hkv * nblk;
+  return ATTN_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -464,6 +566,24 @@ int attn_fwd(const void* q, const void* k, const void* v, void* o, int B, int Hq
 int attn_fwd_stream(const void* q, const void* k, const void* v, void* o, int B, int Hq, int Hkv, int N, int d,
                     int causal, float scale, int mapping, void* cuda_stream) {
   return fwd_impl(q, k, v, o, B, Hq, Hkv, N, d, causal, scale, mapping, reinterpret_cast<cudaStream_t>(cuda_stream));
+}
+
+int attn_fwd_lse(const void* q, const void* k, const void* v, void* o, float* lse, int B, int Hq, int Hkv, int N,
+                 int d, int causal, float scale, int mapping, void* cuda_stream) {
+  if (!lse) return fail(ATTN_ERR_INVALID_VALUE, "null lse");
+  if (B > 0 && Hq > 0 && N > 0 &&
+      (overlaps(lse, (size_t)B * Hq * N * 4, o, (size_t)B * Hq * N * (d > 0 ? d : 0) * 2) ||
+       reinterpret_cast<uintptr_t>(lse) % 4 != 0))
+    return fail(ATTN_ERR_INVALID_VALUE, "lse overlaps o or is misaligned");
+  return fwd_impl(q, k, v, o, B, Hq, Hkv, N, d, causal, scale, mapping, reinterpret_cast<cudaStream_t>(cuda_stream),
+                  lse);
+}
+
+int attn_bwd(const void* q, const void* k, const void* v, const void* o, const void* dout, const float* lse, void* dq,
+             void* dk, void* dv, int B, int Hq, int Hkv, int N, int d, int causal, float scale, int mapping,
+             void* cuda_stream) {
+  return bwd_impl(q, k, v, o, dout, lse, dq, dk, dv, B, Hq, Hkv, N, d, causal, scale, mapping,
+                  reinterpret_cast<cudaStream_t>(cuda_stream));
 }
 
 int attn_fwd_host(const void* q_host, const void* k_host, const void* v_host, void* o_host, int B, int Hq, int Hkv,
@@ -675,6 +795,10 @@ void attn_shutdown(void) {
     cudaSetDevice(dv);
     if (st.d_domain) cudaFree(st.d_domain);
     if (st.d_counters) cudaFree(st.d_counters);
+    if (st.dvec) cudaFree(st.dvec);
+    st.dvec = nullptr;
+    st.dvec_elems = 0;
+    for (bool& a : st.battr_done) a = false;
     for (int i = 0; i < 4; ++i)
       if (st.hbuf[i]) cudaFree(st.hbuf[i]);
     cudaSetDevice(prev);

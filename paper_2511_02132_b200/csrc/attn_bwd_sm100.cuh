@@ -1,0 +1,620 @@
+// attn_bwd_sm100.cuh -- attention backward (eq:ba) on sm_100a.
+//
+//   P  = exp(scale * Q K^T - lse)            (lse from the forward, per query row)
+//   dV = P^T dO            dP = dO V^T        dS = P o (dP - D),  D = rowsum(dO o O)
+//   dQ = scale * dS K      dK = scale * dS^T Q
+//
+// Three kernels, all with the forward's persistent scheduler, so the paper's
+// mappings apply to the backward's work units too ("each
+// workgroup computing different row blocks of the gradients ... may share the
+// same Q, K, V, and dO tensors within the same attention head"):
+//   attn_bwd_dot_kernel   D[b,h,i] = sum_c dO * O                (bandwidth)
+//   attn_bwd_dq_kernel    unit = (b, h, 128-row query block); loops over key
+//                         blocks: S = Q K_j^T and dP = dO V_j^T (SS MMAs) ->
+//                         dS (softmax warps, one query row per thread, bf16
+//                         into TMEM over S) -> dQ += dS K_j (TS MMA).
+//   attn_bwd_dkdv_kernel  unit = (b, kv group g, 128-key block j); loops over
+//                         the group's query heads and query blocks i:
+//                         S^T = K_j Q_i^T and dP^T = V_j dO_i^T (SS MMAs, one
+//                         KEY row per TMEM lane) -> P^T, dS^T (bf16 into TMEM)
+//                         -> dV += P^T dO_i and dK += dS^T Q_i (TS MMAs).
+// Both compute kernels keep every accumulator in TMEM (dQ kernel: S, dP, dQ =
+// 384 columns; dK/dV kernel: S^T, dP^T, dV, dK = 512 columns) and run one
+// 128-row tile per CTA with a serial MMA -> elementwise -> MMA chain per block.
+#pragma once
+#include "attn_fwd_sm100.cuh"
+
+namespace attn {
+namespace bwd {
+
+constexpr int kBM = 128;       // rows of a query block / keys of a key block
+constexpr int kThreads = 256;  // warps 0 TMA, 1 MMA, 2 scheduler + TMEM, 3 idle, 4-7 elementwise
+
+template <int D>
+struct BCfg {
+  static constexpr int kChunks = D / 64;
+  static constexpr int kTile = kBM * D * 2;  // one 128 x D bf16 tile
+  static constexpr int kStages = 2;          // ring depth of the streamed operand pairs
+  static constexpr int kOffA = 0;            // resident pair (dQ: Q, dO;  dKdV: K, V)
+  static constexpr int kOffRing = 2 * kTile;  // ring of streamed pairs (dQ: K, V;  dKdV: Q, dO)
+  static constexpr int kOffVec = kOffRing + kStages * 2 * kTile;  // dKdV: lse/D of each stage
+  static constexpr int kOffCtrl = kOffVec + kStages * 2 * kBM * 4;
+  static constexpr int kSmemBytes = kOffCtrl + 1024 + 1024;
+};
+
+struct BwdParams {
+  int B, Hq, Hkv, N, G, nblk, d_real;
+  float scale, scale_log2;
+  const float* lse;    // [B][Hq][N], natural log
+  const float* dvec;   // [B][Hq][N], rowsum(dO o O)
+  __nv_bfloat16* dq;   // [B][Hq][N][d]
+  __nv_bfloat16* dk;   // [B][Hkv][N][d]
+  __nv_bfloat16* dv;   // [B][Hkv][N][d]
+  SchedParams sched;
+  int U;               // units per "head" of the schedule (query or key blocks)
+  int* counters;
+  const signed char* domain_of_smid;
+  int n_smid;
+};
+
+struct __align__(16) BCtrl {
+  uint64_t sched_full[kSchedRing];
+  uint64_t sched_empty[kSchedRing];
+  uint64_t a_full, a_empty;             // resident pair
+  uint64_t ring_full[4], ring_empty[4]; // streamed pairs
+  uint64_t s_ready, p_ready, o_ready;
+  int4 entry[kSchedRing];
+  uint32_t tmem_base;
+};
+
+// The scheduler warp: identical pop / steal / broadcast protocol as the forward.
+__device__ __forceinline__ void bwd_scheduler(const BwdParams& p, BCtrl* ctrl, int Hsched) {
+  const int sm = (int)ptx::smid();
+  int dom = (sm < p.n_smid) ? (int)p.domain_of_smid[sm] : 0;
+  if (dom < 0) dom = 0;
+  const int nq = p.sched.n_queues;
+  const int q0 = (nq > 1) ? p.sched.queue_of_domain[dom] : 0;
+  uint32_t exhausted = 0;
+  int stage = 0;
+  uint32_t phase = 0;
+  while (true) {
+    int b = 0, h = 0, u = 0, qi = -1;
+    for (int t = 0; t < nq; ++t) {
+      if (t > 0 && !p.sched.steal) break;
+      const int qq = (q0 + t) % nq;
+      if (exhausted & (1u << qq)) continue;
+      const int pos = atomicAdd(&p.counters[qq * 32], 1);
+      if (pos < p.sched.q[qq].len) {
+        decode_unit(p.sched.q[qq], pos, Hsched, p.U, b, h, u);
+        if (p.sched.descending) u = p.U - 1 - u;
+        qi = qq;
+        break;
+      }
+      exhausted |= 1u << qq;
+    }
+    ptx::mbar_wait(&ctrl->sched_empty[stage], phase ^ 1);
+    ctrl->entry[stage] = make_int4(b, h, u, qi >= 0 ? 1 : 0);
+    ptx::mbar_arrive(&ctrl->sched_full[stage]);
+    if (qi < 0) break;
+    if (++stage == kSchedRing) { stage = 0; phase ^= 1; }
+  }
+  __threadfence();
+  if (atomicAdd(&p.counters[kDoneCounter], 1) == (int)gridDim.x - 1) {
+    for (int q = 0; q < nq; ++q) atomicExch(&p.counters[q * 32], 0);
+    atomicExch(&p.counters[kDoneCounter], 0);
+    __threadfence();
+  }
+}
+
+struct BSchedReader {
+  int stage = 0;
+  uint32_t phase = 0;
+  // warp_wide: all 32 lanes call next(); otherwise only the calling lane does.
+  __device__ __forceinline__ int4 next(BCtrl* c, bool warp_wide = true) {
+    ptx::mbar_wait(&c->sched_full[stage], phase);
+    const volatile int* ve = reinterpret_cast<const volatile int*>(&c->entry[stage]);
+    const int4 e = make_int4(ve[0], ve[1], ve[2], ve[3]);
+    if (warp_wide) __syncwarp();
+    if (!warp_wide || (threadIdx.x & 31) == 0) ptx::mbar_arrive(&c->sched_empty[stage]);
+    if (++stage == kSchedRing) { stage = 0; phase ^= 1; }
+    return e;
+  }
+};
+
+// ------------------------------------------------------------------ D = rowsum(dO o O)
+__global__ void attn_bwd_dot_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
+                                    float* __restrict__ dvec, long long rows, int d) {
+  const long long row = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(o + row * d);
+  const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(dout + row * d);
+  float acc = 0.f;
+  for (int c = lane; c < d / 2; c += 32) {
+    const float2 x = __bfloat1622float2(a[c]), y = __bfloat1622float2(b[c]);
+    acc = fmaf(x.x, y.x, fmaf(x.y, y.y, acc));
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (lane == 0) dvec[row] = acc;
+}
+
+// Causal: query block i needs key blocks 0..i;  key block j is needed by query
+// blocks j..nblk-1.  Non-causal: all blocks.
+template <bool kCausal>
+__device__ __forceinline__ int dq_nblocks(int i, int nblk) { return kCausal ? i + 1 : nblk; }
+template <bool kCausal>
+__device__ __forceinline__ int dkdv_first_qblock(int j) { return kCausal ? j : 0; }
+
+// =========================================================================== dQ
+template <int D, bool kCausal>
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
+                       const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                       const BwdParams p) {
+  using C = BCfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sq = smem + C::kOffA;             // Q tile, then dO tile
+  uint8_t* ring = smem + C::kOffRing;        // stage s: K at 2s, V at 2s+1
+  BCtrl* ctrl = reinterpret_cast<BCtrl*>(smem + C::kOffCtrl);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // TMEM: S [0,128), dP [128,256), dQ [256, 256+D)
+  constexpr uint32_t kColS = 0, kColDP = 128, kColDQ = 256;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kSchedRing; ++i) {
+      ptx::mbar_init(&ctrl->sched_full[i], 1);
+      ptx::mbar_init(&ctrl->sched_empty[i], 2 + 4);
+    }
+    ptx::mbar_init(&ctrl->a_full, 1);
+    ptx::mbar_init(&ctrl->a_empty, 1);
+    for (int i = 0; i < C::kStages; ++i) {
+      ptx::mbar_init(&ctrl->ring_full[i], 1);
+      ptx::mbar_init(&ctrl->ring_empty[i], 1);
+    }
+    ptx::mbar_init(&ctrl->s_ready, 1);
+    ptx::mbar_init(&ctrl->p_ready, 4);
+    ptx::mbar_init(&ctrl->o_ready, 1);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) {
+    ptx::tmem_alloc(&ctrl->tmem_base, 512);
+    ptx::tmem_relinquish();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(&ctrl->tmem_base);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      BSchedReader sr;
+      const uint64_t pol_first = ptx::policy_evict_first();
+      const uint64_t pol_kv = ptx::policy_evict_normal();
+      uint32_t a_phase = 0, r_phase = 0;
+      int stage = 0;
+      while (true) {
+        const int4 e = sr.next(ctrl, false);
+        if (!e.w) break;
+        const int b = e.x, h = e.y, i = e.z;
+        const int bh = b * p.Hq + h, kvbh = b * p.Hkv + h / p.G;
+        ptx::mbar_wait(&ctrl->a_empty, a_phase ^ 1);
+        a_phase ^= 1;
+        ptx::mbar_arrive_expect_tx(&ctrl->a_full, 2 * C::kTile);
+#pragma unroll
+        for (int c = 0; c < C::kChunks; ++c) {
+          ptx::tma_load_3d(sq + c * kBM * 128, &tm_q, &ctrl->a_full, c * 64, i * kBM, bh, pol_first);
+          ptx::tma_load_3d(sq + C::kTile + c * kBM * 128, &tm_do, &ctrl->a_full, c * 64, i * kBM, bh, pol_first);
+        }
+        const int n = dq_nblocks<kCausal>(i, p.nblk);
+        for (int j = 0; j < n; ++j) {
+          ptx::mbar_wait(&ctrl->ring_empty[stage], r_phase ^ 1);
+          ptx::mbar_arrive_expect_tx(&ctrl->ring_full[stage], 2 * C::kTile);
+          uint8_t* dst = ring + stage * 2 * C::kTile;
+#pragma unroll
+          for (int c = 0; c < C::kChunks; ++c) {
+            ptx::tma_load_3d(dst + c * kBM * 128, &tm_k, &ctrl->ring_full[stage], c * 64, j * kBM, kvbh, pol_kv);
+            ptx::tma_load_3d(dst + C::kTile + c * kBM * 128, &tm_v, &ctrl->ring_full[stage], c * 64, j * kBM, kvbh,
+                             pol_kv);
+          }
+          if (++stage == C::kStages) { stage = 0; r_phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    BSchedReader sr;
+    constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(kBM, kBM, 0, 0);  // S, dP: K-major A and B
+    constexpr uint32_t idesc_q = ptx::idesc_bf16_f32(kBM, D, 0, 1);    // dQ: A = dS (TMEM), B = K MN-major
+    const uint64_t da0 = ptx::smem_desc_sw128(ptx::smem_u32(sq), 16, 1024);
+    const uint64_t dr0 = ptx::smem_desc_sw128(ptx::smem_u32(ring), 16, 1024);
+    const uint64_t drm0 = ptx::smem_desc_sw128(ptx::smem_u32(ring), kBM * 128, 1024);
+    uint32_t a_phase = 0, r_phase = 0, p_phase = 0;
+    int stage = 0;
+    auto ss_mma = [&](uint32_t d_col, uint64_t a, uint64_t b) {  // [128 x 128] = A[128 x D] B[128 x D]^T
+#pragma unroll
+      for (int k = 0; k < D / 16; ++k) {
+        const uint32_t off = ((k >> 2) * (kBM * 128) + (k & 3) * 32) >> 4;
+        ptx::mma_ss(tmem + d_col, a + off, b + off, idesc_s, k > 0 ? 1u : 0u);
+      }
+    };
+    while (true) {
+      const int4 e = sr.next(ctrl);
+      if (!e.w) break;
+      const int n = dq_nblocks<kCausal>(e.z, p.nblk);
+      ptx::mbar_wait(&ctrl->a_full, a_phase);
+      a_phase ^= 1;
+      int st = stage;
+      ptx::mbar_wait(&ctrl->ring_full[st], r_phase);
+      ptx::tc_fence_after();
+      if (ptx::elect_one_sync()) {
+        const uint64_t kd = dr0 + (uint64_t)((st * 2 * C::kTile) >> 4);
+        ss_mma(kColS, da0, kd);                                                 // S  = Q  K_0^T
+        ss_mma(kColDP, da0 + (uint64_t)(C::kTile >> 4), kd + (uint64_t)(C::kTile >> 4));  // dP = dO V_0^T
+        ptx::mma_commit(&ctrl->s_ready);
+      }
+      __syncwarp();
+      for (int j = 0; j < n; ++j) {
+        ptx::mbar_wait(&ctrl->p_ready, p_phase);
+        p_phase ^= 1;
+        ptx::tc_fence_after();
+        const int cur = st;
+        const bool nxt = j + 1 < n;
+        int nst = cur, nph = r_phase;
+        if (nxt) {
+          nst = cur + 1 == C::kStages ? 0 : cur + 1;
+          nph = cur + 1 == C::kStages ? r_phase ^ 1 : r_phase;
+          ptx::mbar_wait(&ctrl->ring_full[nst], nph);
+          ptx::tc_fence_after();
+        }
+        if (ptx::elect_one_sync()) {
+          // dQ += dS K_j: A = dS (bf16 in TMEM over S), B = K_j as [keys x D] (MN-major)
+          const uint64_t km = drm0 + (uint64_t)((cur * 2 * C::kTile) >> 4);
+#pragma unroll
+          for (int k = 0; k < kBM / 16; ++k)
+            ptx::mma_ts(tmem + kColDQ, tmem + kColS + k * 8, km + (uint64_t)((k * 16 * 128) >> 4), idesc_q,
+                        (j > 0 || k > 0) ? 1u : 0u);
+          ptx::mma_commit(&ctrl->ring_empty[cur]);
+          if (nxt) {
+            const uint64_t kd = dr0 + (uint64_t)((nst * 2 * C::kTile) >> 4);
+            ss_mma(kColS, da0, kd);
+            ss_mma(kColDP, da0 + (uint64_t)(C::kTile >> 4), kd + (uint64_t)(C::kTile >> 4));
+            ptx::mma_commit(&ctrl->s_ready);
+          } else {
+            ptx::mma_commit(&ctrl->a_empty);
+            ptx::mma_commit(&ctrl->o_ready);
+          }
+        }
+        __syncwarp();
+        st = nst;
+        r_phase = nph;
+      }
+      stage = st + 1 == C::kStages ? 0 : st + 1;
+      if (st + 1 == C::kStages) r_phase ^= 1;
+    }
+  } else if (warp == 2) {
+    if (lane == 0) bwd_scheduler(p, ctrl, p.Hq);
+  } else if (warp >= 4) {
+    const int quarter = warp & 3, row = quarter * 32 + lane;
+    const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
+    const float c = p.scale_log2;
+    BSchedReader sr;
+    uint32_t s_phase = 0, o_phase = 0;
+    while (true) {
+      const int4 e = sr.next(ctrl);
+      if (!e.w) break;
+      const int b = e.x, h = e.y, i = e.z;
+      const int qrow = i * kBM + row;
+      const bool valid = qrow < p.N;
+      const long long ridx = (long long)(b * p.Hq + h) * p.N + (valid ? qrow : 0);
+      const float lse2 = valid ? p.lse[ridx] * 1.4426950408889634f : 0.f;
+      const float dd = valid ? p.dvec[ridx] : 0.f;
+      const int n = dq_nblocks<kCausal>(i, p.nblk);
+      for (int j = 0; j < n; ++j) {
+        ptx::mbar_wait(&ctrl->s_ready, s_phase);
+        s_phase ^= 1;
+        ptx::tc_fence_after();
+        // visible keys of this row in block j: k <= lim (causal diagonal, ragged tail)
+        int lim = kBM - 1;
+        if (kCausal && j == i) lim = row;
+        if (j == p.nblk - 1) lim = min(lim, p.N - 1 - j * kBM);
+        if (!valid) lim = -1;
+#pragma unroll
+        for (int cc = 0; cc < kBM; cc += 32) {
+          uint32_t sr_[32], dp[32];
+          ptx::tmem_ld32(trow + kColS + cc, sr_);
+          ptx::tmem_ld32(trow + kColDP + cc, dp);
+          uint32_t pk[16];
+#pragma unroll
+          for (int k = 0; k < 32; k += 2) {
+            float p0 = ptx::ex2(fmaf(__uint_as_float(sr_[k]), c, -lse2));
+            float p1 = ptx::ex2(fmaf(__uint_as_float(sr_[k + 1]), c, -lse2));
+            p0 = (cc + k <= lim) ? p0 : 0.f;
+            p1 = (cc + k + 1 <= lim) ? p1 : 0.f;
+            const float ds0 = p0 * (__uint_as_float(dp[k]) - dd);
+            const float ds1 = p1 * (__uint_as_float(dp[k + 1]) - dd);
+            pk[k >> 1] = ptx::pack_bf16(ds0, ds1);
+          }
+          ptx::tmem_st16(trow + kColS + cc / 2, pk);  // dS (bf16 pairs) over S columns already consumed
+        }
+        ptx::tmem_wait_st();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&ctrl->p_ready);
+      }
+      ptx::mbar_wait(&ctrl->o_ready, o_phase);
+      o_phase ^= 1;
+      ptx::tc_fence_after();
+      __nv_bfloat16* dst = p.dq + ((long long)(b * p.Hq + h) * p.N + (valid ? qrow : 0)) * p.d_real;
+#pragma unroll
+      for (int cc = 0; cc < D; cc += 32) {
+        uint32_t o[32];
+        ptx::tmem_ld32(trow + kColDQ + cc, o);
+        uint32_t pk[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+          pk[k] = ptx::pack_bf16(__uint_as_float(o[2 * k]) * p.scale, __uint_as_float(o[2 * k + 1]) * p.scale);
+        if (valid) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (cc + 8 * k < p.d_real)
+              reinterpret_cast<uint4*>(dst)[cc / 8 + k] = make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
+        }
+      }
+      ptx::tc_fence_before();
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 512);
+  }
+}
+
+// ======================================================================== dK, dV
+template <int D, bool kCausal>
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
+                         const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                         const BwdParams p) {
+  using C = BCfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* skv = smem + C::kOffA;            // K tile, then V tile
+  uint8_t* ring = smem + C::kOffRing;        // stage s: Q at 2s, dO at 2s+1
+  BCtrl* ctrl = reinterpret_cast<BCtrl*>(smem + C::kOffCtrl);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // TMEM: S^T [0,128), dP^T [128,256), dV [256, 256+D), dK [384, 384+D)
+  constexpr uint32_t kColS = 0, kColDP = 128, kColDV = 256, kColDK = 384;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kSchedRing; ++i) {
+      ptx::mbar_init(&ctrl->sched_full[i], 1);
+      ptx::mbar_init(&ctrl->sched_empty[i], 2 + 4);
+    }
+    ptx::mbar_init(&ctrl->a_full, 1);
+    ptx::mbar_init(&ctrl->a_empty, 1);
+    for (int i = 0; i < C::kStages; ++i) {
+      ptx::mbar_init(&ctrl->ring_full[i], 1);
+      ptx::mbar_init(&ctrl->ring_empty[i], 1);
+    }
+    ptx::mbar_init(&ctrl->s_ready, 1);
+    ptx::mbar_init(&ctrl->p_ready, 4);
+    ptx::mbar_init(&ctrl->o_ready, 1);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) {
+    ptx::tmem_alloc(&ctrl->tmem_base, 512);
+    ptx::tmem_relinquish();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(&ctrl->tmem_base);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      BSchedReader sr;
+      const uint64_t pol_kv = ptx::policy_evict_first();
+      const uint64_t pol_q = ptx::policy_evict_normal();
+      uint32_t a_phase = 0, r_phase = 0;
+      int stage = 0;
+      while (true) {
+        const int4 e = sr.next(ctrl, false);
+        if (!e.w) break;
+        const int b = e.x, g = e.y, j = e.z;
+        const int kvbh = b * p.Hkv + g;
+        ptx::mbar_wait(&ctrl->a_empty, a_phase ^ 1);
+        a_phase ^= 1;
+        ptx::mbar_arrive_expect_tx(&ctrl->a_full, 2 * C::kTile);
+#pragma unroll
+        for (int c = 0; c < C::kChunks; ++c) {
+          ptx::tma_load_3d(skv + c * kBM * 128, &tm_k, &ctrl->a_full, c * 64, j * kBM, kvbh, pol_kv);
+          ptx::tma_load_3d(skv + C::kTile + c * kBM * 128, &tm_v, &ctrl->a_full, c * 64, j * kBM, kvbh, pol_kv);
+        }
+        for (int hh = 0; hh < p.G; ++hh) {
+          const int bh = b * p.Hq + g * p.G + hh;
+          for (int i = dkdv_first_qblock<kCausal>(j); i < p.nblk; ++i) {
+            ptx::mbar_wait(&ctrl->ring_empty[stage], r_phase ^ 1);
+            ptx::mbar_arrive_expect_tx(&ctrl->ring_full[stage], 2 * C::kTile);
+            uint8_t* dst = ring + stage * 2 * C::kTile;
+#pragma unroll
+            for (int c = 0; c < C::kChunks; ++c) {
+              ptx::tma_load_3d(dst + c * kBM * 128, &tm_q, &ctrl->ring_full[stage], c * 64, i * kBM, bh, pol_q);
+              ptx::tma_load_3d(dst + C::kTile + c * kBM * 128, &tm_do, &ctrl->ring_full[stage], c * 64, i * kBM, bh,
+                               pol_q);
+            }
+            if (++stage == C::kStages) { stage = 0; r_phase ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    BSchedReader sr;
+    constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(kBM, kBM, 0, 0);  // S^T, dP^T
+    constexpr uint32_t idesc_g = ptx::idesc_bf16_f32(kBM, D, 0, 1);    // dV, dK: A in TMEM, B MN-major
+    const uint64_t dkv0 = ptx::smem_desc_sw128(ptx::smem_u32(skv), 16, 1024);
+    const uint64_t dr0 = ptx::smem_desc_sw128(ptx::smem_u32(ring), 16, 1024);
+    const uint64_t drm0 = ptx::smem_desc_sw128(ptx::smem_u32(ring), kBM * 128, 1024);
+    uint32_t a_phase = 0, r_phase = 0, p_phase = 0;
+    int stage = 0;
+    auto ss_mma = [&](uint32_t d_col, uint64_t a, uint64_t b) {
+#pragma unroll
+      for (int k = 0; k < D / 16; ++k) {
+        const uint32_t off = ((k >> 2) * (kBM * 128) + (k & 3) * 32) >> 4;
+        ptx::mma_ss(tmem + d_col, a + off, b + off, idesc_s, k > 0 ? 1u : 0u);
+      }
+    };
+    while (true) {
+      const int4 e = sr.next(ctrl);
+      if (!e.w) break;
+      const int n = p.G * (p.nblk - dkdv_first_qblock<kCausal>(e.z));
+      ptx::mbar_wait(&ctrl->a_full, a_phase);
+      a_phase ^= 1;
+      int st = stage;
+      ptx::mbar_wait(&ctrl->ring_full[st], r_phase);
+      ptx::tc_fence_after();
+      if (ptx::elect_one_sync()) {
+        const uint64_t qd = dr0 + (uint64_t)((st * 2 * C::kTile) >> 4);
+        ss_mma(kColS, dkv0, qd);                                                            // S^T  = K Q_i^T
+        ss_mma(kColDP, dkv0 + (uint64_t)(C::kTile >> 4), qd + (uint64_t)(C::kTile >> 4));   // dP^T = V dO_i^T
+        ptx::mma_commit(&ctrl->s_ready);
+      }
+      __syncwarp();
+      for (int it = 0; it < n; ++it) {
+        ptx::mbar_wait(&ctrl->p_ready, p_phase);
+        p_phase ^= 1;
+        ptx::tc_fence_after();
+        const int cur = st;
+        const bool nxt = it + 1 < n;
+        int nst = cur, nph = r_phase;
+        if (nxt) {
+          nst = cur + 1 == C::kStages ? 0 : cur + 1;
+          nph = cur + 1 == C::kStages ? r_phase ^ 1 : r_phase;
+          ptx::mbar_wait(&ctrl->ring_full[nst], nph);
+          ptx::tc_fence_after();
+        }
+        if (ptx::elect_one_sync()) {
+          const uint64_t qm = drm0 + (uint64_t)((cur * 2 * C::kTile) >> 4);  // Q_i as [queries x D] MN-major
+          const uint64_t dom = qm + (uint64_t)(C::kTile >> 4);               // dO_i likewise
+#pragma unroll
+          for (int k = 0; k < kBM / 16; ++k) {
+            ptx::mma_ts(tmem + kColDV, tmem + kColS + k * 8, dom + (uint64_t)((k * 16 * 128) >> 4), idesc_g,
+                        (it > 0 || k > 0) ? 1u : 0u);   // dV += P^T dO_i
+            ptx::mma_ts(tmem + kColDK, tmem + kColDP + k * 8, qm + (uint64_t)((k * 16 * 128) >> 4), idesc_g,
+                        (it > 0 || k > 0) ? 1u : 0u);   // dK += dS^T Q_i
+          }
+          ptx::mma_commit(&ctrl->ring_empty[cur]);
+          if (nxt) {
+            const uint64_t qd = dr0 + (uint64_t)((nst * 2 * C::kTile) >> 4);
+            ss_mma(kColS, dkv0, qd);
+            ss_mma(kColDP, dkv0 + (uint64_t)(C::kTile >> 4), qd + (uint64_t)(C::kTile >> 4));
+            ptx::mma_commit(&ctrl->s_ready);
+          } else {
+            ptx::mma_commit(&ctrl->a_empty);
+            ptx::mma_commit(&ctrl->o_ready);
+          }
+        }
+        __syncwarp();
+        st = nst;
+        r_phase = nph;
+      }
+      stage = st + 1 == C::kStages ? 0 : st + 1;
+      if (st + 1 == C::kStages) r_phase ^= 1;
+    }
+  } else if (warp == 2) {
+    if (lane == 0) bwd_scheduler(p, ctrl, p.Hkv);
+  } else if (warp >= 4) {
+    const int quarter = warp & 3, krow = quarter * 32 + lane;  // key row of the block
+    const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
+    const float c = p.scale_log2;
+    BSchedReader sr;
+    uint32_t s_phase = 0, o_phase = 0;
+    while (true) {
+      const int4 e = sr.next(ctrl);
+      if (!e.w) break;
+      const int b = e.x, g = e.y, j = e.z;
+      const int kglob = j * kBM + krow;
+      const int i0 = dkdv_first_qblock<kCausal>(j);
+      for (int hh = 0; hh < p.G; ++hh) {
+        for (int i = i0; i < p.nblk; ++i) {
+          ptx::mbar_wait(&ctrl->s_ready, s_phase);
+          s_phase ^= 1;
+          ptx::tc_fence_after();
+          // lse / D of this block's 128 queries: warp-broadcast loads (L2-resident)
+          const long long vi = (long long)(b * p.Hq + g * p.G + hh) * p.N + i * kBM;
+          // visible queries of this key: q >= k (causal), q < N; local query index qq
+          int qlo = 0, qhi = kBM - 1;
+          if (kCausal && i == j) qlo = krow;           // query >= key
+          if (i == p.nblk - 1) qhi = p.N - 1 - i * kBM;  // ragged tail
+#pragma unroll
+          for (int cc = 0; cc < kBM; cc += 32) {
+            uint32_t sr_[32], dp[32];
+            ptx::tmem_ld32(trow + kColS + cc, sr_);
+            ptx::tmem_ld32(trow + kColDP + cc, dp);
+            uint32_t pp[16], pd[16];
+#pragma unroll
+            for (int k = 0; k < 32; k += 2) {
+              const int q0 = cc + k, q1 = cc + k + 1;
+              const bool v0 = q0 >= qlo && q0 <= qhi, v1 = q1 >= qlo && q1 <= qhi;
+              const float l0 = v0 ? __ldg(p.lse + vi + q0) * 1.4426950408889634f : 0.f;
+              const float l1 = v1 ? __ldg(p.lse + vi + q1) * 1.4426950408889634f : 0.f;
+              const float d0 = v0 ? __ldg(p.dvec + vi + q0) : 0.f;
+              const float d1 = v1 ? __ldg(p.dvec + vi + q1) : 0.f;
+              float p0 = ptx::ex2(fmaf(__uint_as_float(sr_[k]), c, -l0));
+              float p1 = ptx::ex2(fmaf(__uint_as_float(sr_[k + 1]), c, -l1));
+              p0 = v0 ? p0 : 0.f;
+              p1 = v1 ? p1 : 0.f;
+              pp[k >> 1] = ptx::pack_bf16(p0, p1);
+              pd[k >> 1] = ptx::pack_bf16(p0 * (__uint_as_float(dp[k]) - d0), p1 * (__uint_as_float(dp[k + 1]) - d1));
+            }
+            ptx::tmem_st16(trow + kColS + cc / 2, pp);   // P^T over consumed S^T columns
+            ptx::tmem_st16(trow + kColDP + cc / 2, pd);  // dS^T over consumed dP^T columns
+          }
+          ptx::tmem_wait_st();
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&ctrl->p_ready);
+        }
+      }
+      ptx::mbar_wait(&ctrl->o_ready, o_phase);
+      o_phase ^= 1;
+      ptx::tc_fence_after();
+      const bool valid = kglob < p.N;
+      const long long ro = ((long long)(b * p.Hkv + g) * p.N + (valid ? kglob : 0)) * p.d_real;
+#pragma unroll
+      for (int which = 0; which < 2; ++which) {
+        __nv_bfloat16* dst = (which == 0 ? p.dv : p.dk) + ro;
+        const float f = which == 0 ? 1.f : p.scale;
+        const uint32_t col = which == 0 ? kColDV : kColDK;
+#pragma unroll
+        for (int cc = 0; cc < D; cc += 32) {
+          uint32_t o[32];
+          ptx::tmem_ld32(trow + col + cc, o);
+          uint32_t pk[16];
+#pragma unroll
+          for (int k = 0; k < 16; ++k)
+            pk[k] = ptx::pack_bf16(__uint_as_float(o[2 * k]) * f, __uint_as_float(o[2 * k + 1]) * f);
+          if (valid) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              if (cc + 8 * k < p.d_real)
+                reinterpret_cast<uint4*>(dst)[cc / 8 + k] =
+                    make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
+          }
+        }
+      }
+      ptx::tc_fence_before();
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 512);
+  }
+}
+
+}  // namespace bwd
+}  // namespace attn

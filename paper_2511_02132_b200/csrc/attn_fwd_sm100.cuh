@@ -101,6 +101,7 @@ struct KernelParams {
   int d_real;        // head dim of the tensors (<= D; TMA zero-fills columns d_real..D-1)
   float scale_log2;  // scale * log2(e), >= 0
   __nv_bfloat16* o;
+  float* lse;        // optional [B][Hq][N] natural-log row LSE (backward input), may be null
   SchedParams sched;
   int* counters;                 // one int per queue, 32 ints apart, then the done count
   const signed char* domain_of_smid;
@@ -642,6 +643,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       o_phase ^= 1;
       ptx::tc_fence_after();
       const float inv_l = 1.f / l;
+      if (p.lse != nullptr && hf == 0 && qb * kBlockM + row < p.N)  // lse = scale*m + ln(l)
+        p.lse[(long long)(e.x * p.Hq + e.y) * p.N + qb * kBlockM + row] = (m * c + __log2f(l)) * 0.6931471805599453f;
       const long long orow = ((long long)(e.x * p.Hq + e.y) * p.N + (long long)qb * kBlockM + row) * p.d_real;
       uint4* dst = reinterpret_cast<uint4*>(p.o + orow + hf * kOCols);
       // real columns of this thread's slice (multiple of 8); rows >= N (ragged
