@@ -37,7 +37,7 @@ struct BCfg {
   static constexpr int kStages = 2;          // ring depth of the streamed operand pairs
   static constexpr int kOffA = 0;            // resident pair (dQ: Q, dO;  dKdV: K, V)
   static constexpr int kOffRing = 2 * kTile;  // ring of streamed pairs (dQ: K, V;  dKdV: Q, dO)
-  static constexpr int kOffVec = kOffRing + kStages * 2 * kTile;  // dKdV: lse/D of each stage
+  static constexpr int kOffVec = kOffRing + kStages * 2 * kTile;  // dKdV: staged lse2 / D (2 parities)
   static constexpr int kOffCtrl = kOffVec + kStages * 2 * kBM * 4;
   static constexpr int kSmemBytes = kOffCtrl + 1024 + 1024;
 };
@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (kCausal && j == i) lim = row;
         if (j == p.nblk - 1) lim = min(lim, p.N - 1 - j * kBM);
         if (!valid) lim = -1;
-#pragma unroll
+#pragma unroll 1
         for (int cc = 0; cc < kBM; cc += 32) {
           uint32_t sr_[32], dp[32];
           ptx::tmem_ld32(trow + kColS + cc, sr_);
@@ -530,7 +530,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
     const float c = p.scale_log2;
     BSchedReader sr;
-    uint32_t s_phase = 0, o_phase = 0;
+    uint32_t s_phase = 0, o_phase = 0, blk = 0;
+    float* svec = reinterpret_cast<float*>(smem + C::kOffVec);  // [parity][lse2 | D]
     while (true) {
       const int4 e = sr.next(ctrl);
       if (!e.w) break;
@@ -542,32 +543,44 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::mbar_wait(&ctrl->s_ready, s_phase);
           s_phase ^= 1;
           ptx::tc_fence_after();
-          // lse / D of this block's 128 queries: warp-broadcast loads (L2-resident)
+          // lse (as log2) and D of this block's 128 queries, staged in SMEM by the
+          // 128 elementwise threads (double-buffered by block parity)
           const long long vi = (long long)(b * p.Hq + g * p.G + hh) * p.N + i * kBM;
+          float* sv = svec + (blk & 1) * 2 * kBM;
+          {
+            const bool ok = i * kBM + krow < p.N;
+            sv[krow] = ok ? __ldg(p.lse + vi + krow) * 1.4426950408889634f : 0.f;
+            sv[kBM + krow] = ok ? __ldg(p.dvec + vi + krow) : 0.f;
+            ptx::named_bar_sync(1, 128);
+          }
+          ++blk;
           // visible queries of this key: q >= k (causal), q < N; local query index qq
           int qlo = 0, qhi = kBM - 1;
           if (kCausal && i == j) qlo = krow;           // query >= key
           if (i == p.nblk - 1) qhi = p.N - 1 - i * kBM;  // ragged tail
-#pragma unroll
+#pragma unroll 1
           for (int cc = 0; cc < kBM; cc += 32) {
             uint32_t sr_[32], dp[32];
             ptx::tmem_ld32(trow + kColS + cc, sr_);
             ptx::tmem_ld32(trow + kColDP + cc, dp);
             uint32_t pp[16], pd[16];
 #pragma unroll
-            for (int k = 0; k < 32; k += 2) {
-              const int q0 = cc + k, q1 = cc + k + 1;
-              const bool v0 = q0 >= qlo && q0 <= qhi, v1 = q1 >= qlo && q1 <= qhi;
-              const float l0 = v0 ? __ldg(p.lse + vi + q0) * 1.4426950408889634f : 0.f;
-              const float l1 = v1 ? __ldg(p.lse + vi + q1) * 1.4426950408889634f : 0.f;
-              const float d0 = v0 ? __ldg(p.dvec + vi + q0) : 0.f;
-              const float d1 = v1 ? __ldg(p.dvec + vi + q1) : 0.f;
-              float p0 = ptx::ex2(fmaf(__uint_as_float(sr_[k]), c, -l0));
-              float p1 = ptx::ex2(fmaf(__uint_as_float(sr_[k + 1]), c, -l1));
-              p0 = v0 ? p0 : 0.f;
-              p1 = v1 ? p1 : 0.f;
-              pp[k >> 1] = ptx::pack_bf16(p0, p1);
-              pd[k >> 1] = ptx::pack_bf16(p0 * (__uint_as_float(dp[k]) - d0), p1 * (__uint_as_float(dp[k + 1]) - d1));
+            for (int k = 0; k < 32; k += 4) {
+              const float4 l4 = *reinterpret_cast<const float4*>(sv + cc + k);
+              const float4 d4 = *reinterpret_cast<const float4*>(sv + kBM + cc + k);
+              const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dvv[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+              for (int u = 0; u < 4; u += 2) {
+                const int q0 = cc + k + u, q1 = q0 + 1;
+                const bool v0 = q0 >= qlo && q0 <= qhi, v1 = q1 >= qlo && q1 <= qhi;
+                float p0 = ptx::ex2(fmaf(__uint_as_float(sr_[k + u]), c, -lv[u]));
+                float p1 = ptx::ex2(fmaf(__uint_as_float(sr_[k + u + 1]), c, -lv[u + 1]));
+                p0 = v0 ? p0 : 0.f;
+                p1 = v1 ? p1 : 0.f;
+                pp[(k + u) >> 1] = ptx::pack_bf16(p0, p1);
+                pd[(k + u) >> 1] = ptx::pack_bf16(p0 * (__uint_as_float(dp[k + u]) - dvv[u]),
+                                                  p1 * (__uint_as_float(dp[k + u + 1]) - dvv[u + 1]));
+              }
             }
             ptx::tmem_st16(trow + kColS + cc / 2, pp);   // P^T over consumed S^T columns
             ptx::tmem_st16(trow + kColDP + cc / 2, pd);  // dS^T over consumed dP^T columns
