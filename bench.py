@@ -38,9 +38,11 @@ METRIC = "attention fwd TFLOP/s (% of bf16 peak) and L2 hit rate by mapping, 1/2
 MAPS = ("block_first", "head_first", "swizzled_head_first", "swizzled_block_first")
 
 
-def flops_fwd(B, Hq, N, d, causal) -> float:
-    """4*B*Hq*N^2*d (two matmuls, eq:fa); causal counts half (FA convention, R14)."""
-    f = 4.0 * B * Hq * N * N * d
+def flops_fwd(B, Hq, N, d, causal, pass_="fwd") -> float:
+    """4*B*Hq*N^2*d (two matmuls, eq:fa); the backward counts five matmuls,
+    10*B*Hq*N^2*d (eq:ba); causal counts half (FA convention,
+    DESIGN.md R14)."""
+    f = (10.0 if pass_ == "bwd" else 4.0) * B * Hq * N * N * d
     return f * 0.5 if causal else f
 
 
@@ -156,12 +158,22 @@ def run_ours(a):
     l2_note += "; L2 flushed (memset 2xL2) before every step, outside the per-launch events" if a.flush else "; no flush"
     flush_buf = torch.empty(2 * l2, dtype=torch.uint8, device=dev) if a.flush else None
     stream = torch.cuda.current_stream()
-    flops_rank = flops_fwd(B, hq, N, d, causal)
-    flops_job = flops_fwd(B, Hq_job, N, d, causal)
+    flops_rank = flops_fwd(B, hq, N, d, causal, a.pass_)
+    flops_job = flops_fwd(B, Hq_job, N, d, causal, a.pass_)
+    bwd_inputs = []
+    if a.pass_ == "bwd":  # forward once (untimed) for O and the row LSE; dO seeded like Q
+        for s_, (q, k, v, o) in enumerate(sets):
+            o2, lse = api.attn_fwd_lse(q, k, v, causal=causal, scale=scale)
+            do = synth.make_tensor("q", B, hq, N, d, base=100 + s_, head_offset=shard.q_lo, device=dev)
+            bwd_inputs.append((o2, lse, do))
 
     def step(i, mapping):
         q, k, v, o = sets[i % n_sets]
-        api.attn_fwd(q, k, v, o, causal=causal, scale=scale, mapping=mapping, stream=stream)
+        if a.pass_ == "bwd":
+            o2, lse, do = bwd_inputs[i % n_sets]
+            api.attn_bwd(q, k, v, o2, do, lse, causal=causal, scale=scale, mapping=mapping, stream=stream)
+        else:
+            api.attn_fwd(q, k, v, o, causal=causal, scale=scale, mapping=mapping, stream=stream)
 
     def timed(mapping, steps, warmup, sampler=None):
         for i in range(warmup):
@@ -204,11 +216,11 @@ def run_ours(a):
             msm = ms_step
         else:
             msm, _, _ = timed(m, max(3, a.steps // 4), 2)
-        prof = load_profile_summary(a.workload, m)
+        prof = load_profile_summary(a.workload, m) if a.pass_ == "fwd" else None
         by_mapping[m] = {"tflops": round(flops_job / (msm * 1e-3) / 1e12, 1), "ms_per_step": round(msm, 4),
                          "l2_hit_rate_pct": prof.get("lts__t_sector_hit_rate.pct") if prof else None}
 
-    # end to end through the public API on pinned host buffers
+    # end to end through the public API on pinned host buffers (forward)
     qh, kh, vh, _ = sets[0]
     qh, kh, vh = (t.cpu().pin_memory() for t in (qh, kh, vh))
     oh = torch.empty_like(qh).pin_memory()
@@ -226,16 +238,17 @@ def run_ours(a):
 
     peak, peak_sus, peak_src = load_peaks()
     achieved = flops_rank / (ms_kernel * 1e-3) / 1e12
-    prof = load_profile_summary(a.workload, a.mapping)
+    prof = load_profile_summary(a.workload, a.mapping) if a.pass_ == "fwd" else None
     traffic = None
     if prof and prof.get("dram_bytes_per_launch") is not None:
         traffic = prof["dram_bytes_per_launch"]
     out = {
-        "metric": METRIC, "value": round(value, 2), "unit": "TFLOP/s", "n_gpus": world, "steps": a.steps,
+        "metric": METRIC if a.pass_ == "fwd" else METRIC.replace("attention fwd", "attention bwd"),
+        "value": round(value, 2), "unit": "TFLOP/s", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (i.i.d. N(0,1) rounded to bf16, seeded per head)",
         "config": {"workload": a.workload, "B": B, "Hq": Hq_job, "Hkv": Hkv_job, "N": N, "d": d, "causal": causal,
-                   "mapping": a.mapping, "heads_per_gpu": hq,
+                   "mapping": a.mapping, "pass": a.pass_, "heads_per_gpu": hq,
                    "parallelism": f"heads sharded over {world} GPU(s), no data-path collective",
                    "l2": l2_note, "flop_convention": "4*B*Hq*N^2*d, causal x0.5"},
         "roofline": {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
@@ -252,7 +265,7 @@ def run_ours(a):
         "gpu_launches": launches,
         "clocks": clocks,
     }
-    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+    if rank == 0 and world == 1 and not a.no_cpu_baseline and a.pass_ == "fwd":
         out["cpu_baseline"] = cpu_baseline(a.workload, a.cpu_seconds)
     if rank == 0:
         print(json.dumps(out), flush=True)
@@ -374,6 +387,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--sets", type=int, default=0, help="resident input sets rotated per step (0: auto)")
     ap.add_argument("--flush", action="store_true", help="memset a 2xL2 buffer before every step")
+    ap.add_argument("--pass", dest="pass_", default="fwd", choices=("fwd", "bwd"),
+                    help="time the forward (default, the headline) or the backward (NEXT-3)")
     a = ap.parse_args()
     if a.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
