@@ -59,8 +59,14 @@ def env_rank_world():
 
 
 def init(backend: Optional[str] = None) -> tuple:
-    """Initialise the default process group from torchrun's env (127.0.0.1 rendezvous)."""
+    """Initialise the default process group from torchrun's env (127.0.0.1 rendezvous).
+
+    ATTN_BENCH_SHARE_GPU=1 (tests only): every rank uses cuda:0 and gloo, so
+    the multi-rank code path can be exercised on a one-GPU box."""
     rank, world, local = env_rank_world()
+    if os.environ.get("ATTN_BENCH_SHARE_GPU") == "1":
+        local = 0
+        backend = "gloo"
     if world > 1 and not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         if backend is None:
@@ -88,6 +94,8 @@ def max_over_ranks(x: float, device=None) -> float:
     """Max of a scalar over all ranks (timing aggregation)."""
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return float(x)
+    if dist.get_backend() != "nccl":
+        device = "cpu"
     t = torch.tensor([float(x)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
