@@ -471,9 +471,9 @@ int launch_bwd_t(DevState& st, const CUtensorMap& tq, const CUtensorMap& tdo, co
     ATTN_CUDA(cudaFuncSetAttribute(kkv, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     st.battr_done[idx] = true;
   }
-  kq<<<grid_q, bwd::kThreads, smem, s>>>(tq, tdo, tk, tv, pq);
+  kq<<<grid_q, bwd::kThreadsKV, smem, s>>>(tq, tdo, tk, tv, pq);
   ATTN_CUDA(cudaGetLastError());
-  kkv<<<grid_kv, bwd::kThreads, smem, s>>>(tq, tdo, tk, tv, pkv);
+  kkv<<<grid_kv, bwd::kThreadsKV, smem, s>>>(tq, tdo, tk, tv, pkv);
   ATTN_CUDA(cudaGetLastError());
   return ATTN_OK;
 }

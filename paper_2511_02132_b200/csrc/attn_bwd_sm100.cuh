@@ -11,8 +11,9 @@
 //   attn_bwd_dot_kernel   D[b,h,i] = sum_c dO * O                (bandwidth)
 //   attn_bwd_dq_kernel    unit = (b, h, 128-row query block); loops over key
 //                         blocks: S = Q K_j^T and dP = dO V_j^T (SS MMAs) ->
-//                         dS (softmax warps, one query row per thread, bf16
-//                         into TMEM over S) -> dQ += dS K_j (TS MMA).
+//                         P (registers), dS (8 elementwise warps: TMEM lane =
+//                         query row, two key halves; bf16 into TMEM over dP)
+//                         -> dQ += dS K_j (TS MMA).
 //   attn_bwd_dkdv_kernel  unit = (b, kv group g, 128-key block j); loops over
 //                         the group's query heads and query blocks i:
 //                         S^T = K_j Q_i^T and dP^T = V_j dO_i^T (SS MMAs, one
@@ -20,7 +21,9 @@
 //                         -> dV += P^T dO_i and dK += dS^T Q_i (TS MMAs).
 // Both compute kernels keep every accumulator in TMEM (dQ kernel: S, dP, dQ =
 // 384 columns; dK/dV kernel: S^T, dP^T, dV, dK = 512 columns) and run one
-// 128-row tile per CTA with a serial MMA -> elementwise -> MMA chain per block.
+// 128-row tile per CTA.  Both split the elementwise work into a P phase (from
+// S) and a dS phase (from dP) interleaved with the MMAs (see the MMA warps),
+// so the tensor pipe keeps working while the exps run.
 #pragma once
 #include "attn_fwd_sm100.cuh"
 
@@ -28,7 +31,7 @@ namespace attn {
 namespace bwd {
 
 constexpr int kBM = 128;       // rows of a query block / keys of a key block
-constexpr int kThreads = 256;  // warps 0 TMA, 1 MMA, 2 scheduler + TMEM, 3 idle, 4-7 elementwise
+constexpr int kThreadsKV = 384;  // warps 0 TMA, 1 MMA, 2 scheduler + TMEM, 3 idle, 4-11 elementwise (two column halves)
 
 template <int D>
 struct BCfg {
@@ -63,6 +66,7 @@ struct __align__(16) BCtrl {
   uint64_t a_full, a_empty;             // resident pair
   uint64_t ring_full[4], ring_empty[4]; // streamed pairs
   uint64_t s_ready, p_ready, o_ready;
+  uint64_t dp_ready, ds_ready;          // dKdV: dP^T in TMEM, dS^T stored
   int4 entry[kSchedRing];
   uint32_t tmem_base;
 };
@@ -148,7 +152,7 @@ __device__ __forceinline__ int dkdv_first_qblock(int j) { return kCausal ? j : 0
 
 // =========================================================================== dQ
 template <int D, bool kCausal>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreadsKV, 1)
     attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                        const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                        const BwdParams p) {
@@ -161,11 +165,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // TMEM: S [0,128), dP [128,256), dQ [256, 256+D)
   constexpr uint32_t kColS = 0, kColDP = 128, kColDQ = 256;
+  constexpr int kEw = 8;  // elementwise warps
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kSchedRing; ++i) {
       ptx::mbar_init(&ctrl->sched_full[i], 1);
-      ptx::mbar_init(&ctrl->sched_empty[i], 2 + 4);
+      ptx::mbar_init(&ctrl->sched_empty[i], 2 + kEw);
     }
     ptx::mbar_init(&ctrl->a_full, 1);
     ptx::mbar_init(&ctrl->a_empty, 1);
@@ -174,7 +179,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(&ctrl->ring_empty[i], 1);
     }
     ptx::mbar_init(&ctrl->s_ready, 1);
-    ptx::mbar_init(&ctrl->p_ready, 4);
+    ptx::mbar_init(&ctrl->dp_ready, 1);
+    ptx::mbar_init(&ctrl->p_ready, kEw);   // S consumed (P held in registers)
+    ptx::mbar_init(&ctrl->ds_ready, kEw);
     ptx::mbar_init(&ctrl->o_ready, 1);
     ptx::fence_barrier_init();
   }
@@ -223,6 +230,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
+    // Per block j the tensor pipe runs  S(j+1) . dQ(j) . dP(j+1):  S(j+1) is
+    // issued as soon as the elementwise warps have read S(j) (P stays in their
+    // registers), so the exps of block j+1 overlap dQ(j) and dP(j+1).
     BSchedReader sr;
     constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(kBM, kBM, 0, 0);  // S, dP: K-major A and B
     constexpr uint32_t idesc_q = ptx::idesc_bf16_f32(kBM, D, 0, 1);    // dQ: A = dS (TMEM), B = K MN-major
@@ -250,36 +260,47 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (ptx::elect_one_sync()) {
         const uint64_t kd = dr0 + (uint64_t)((st * 2 * C::kTile) >> 4);
         ss_mma(kColS, da0, kd);                                                 // S  = Q  K_0^T
-        ss_mma(kColDP, da0 + (uint64_t)(C::kTile >> 4), kd + (uint64_t)(C::kTile >> 4));  // dP = dO V_0^T
         ptx::mma_commit(&ctrl->s_ready);
+        ss_mma(kColDP, da0 + (uint64_t)(C::kTile >> 4), kd + (uint64_t)(C::kTile >> 4));  // dP = dO V_0^T
+        ptx::mma_commit(&ctrl->dp_ready);
       }
       __syncwarp();
       for (int j = 0; j < n; ++j) {
-        ptx::mbar_wait(&ctrl->p_ready, p_phase);
-        p_phase ^= 1;
-        ptx::tc_fence_after();
         const int cur = st;
         const bool nxt = j + 1 < n;
         int nst = cur, nph = r_phase;
         if (nxt) {
           nst = cur + 1 == C::kStages ? 0 : cur + 1;
           nph = cur + 1 == C::kStages ? r_phase ^ 1 : r_phase;
+        }
+        const uint64_t kd = dr0 + (uint64_t)((nst * 2 * C::kTile) >> 4);
+        ptx::mbar_wait(&ctrl->p_ready, p_phase);   // S(j) read
+        ptx::tc_fence_after();
+        if (nxt) {
           ptx::mbar_wait(&ctrl->ring_full[nst], nph);
           ptx::tc_fence_after();
+          if (ptx::elect_one_sync()) {
+            ss_mma(kColS, da0, kd);                 // S(j+1)
+            ptx::mma_commit(&ctrl->s_ready);
+          }
+          __syncwarp();
         }
+        ptx::mbar_wait(&ctrl->ds_ready, p_phase);
+        p_phase ^= 1;
+        ptx::tc_fence_after();
         if (ptx::elect_one_sync()) {
-          // dQ += dS K_j: A = dS (bf16 in TMEM over S), B = K_j as [keys x D] (MN-major)
+          // dQ += dS K_j: A = dS (bf16 in TMEM over dP; queries' keys 0-63 in
+          // columns [0,32), keys 64-127 in [64,96) of the region), B = K_j as
+          // [keys x D] (MN-major)
           const uint64_t km = drm0 + (uint64_t)((cur * 2 * C::kTile) >> 4);
 #pragma unroll
           for (int k = 0; k < kBM / 16; ++k)
-            ptx::mma_ts(tmem + kColDQ, tmem + kColS + k * 8, km + (uint64_t)((k * 16 * 128) >> 4), idesc_q,
-                        (j > 0 || k > 0) ? 1u : 0u);
+            ptx::mma_ts(tmem + kColDQ, tmem + kColDP + k * 8 + (k >= 4 ? 32 : 0),
+                        km + (uint64_t)((k * 16 * 128) >> 4), idesc_q, (j > 0 || k > 0) ? 1u : 0u);
           ptx::mma_commit(&ctrl->ring_empty[cur]);
           if (nxt) {
-            const uint64_t kd = dr0 + (uint64_t)((nst * 2 * C::kTile) >> 4);
-            ss_mma(kColS, da0, kd);
-            ss_mma(kColDP, da0 + (uint64_t)(C::kTile >> 4), kd + (uint64_t)(C::kTile >> 4));
-            ptx::mma_commit(&ctrl->s_ready);
+            ss_mma(kColDP, da0 + (uint64_t)(C::kTile >> 4), kd + (uint64_t)(C::kTile >> 4));  // dP(j+1)
+            ptx::mma_commit(&ctrl->dp_ready);
           } else {
             ptx::mma_commit(&ctrl->a_empty);
             ptx::mma_commit(&ctrl->o_ready);
@@ -295,7 +316,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 2) {
     if (lane == 0) bwd_scheduler(p, ctrl, p.Hq);
   } else if (warp >= 4) {
+    // 256 threads: TMEM lane = query row (warp & 3), column half `half` =
+    // keys [64*half, 64*half+64) of each block.
     const int quarter = warp & 3, row = quarter * 32 + lane;
+    const int half = (warp - 4) >> 2, k0c = half * 64;
     const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
     const float c = p.scale_log2;
     BSchedReader sr;
@@ -311,43 +335,52 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float dd = valid ? p.dvec[ridx] : 0.f;
       const int n = dq_nblocks<kCausal>(i, p.nblk);
       for (int j = 0; j < n; ++j) {
-        ptx::mbar_wait(&ctrl->s_ready, s_phase);
-        s_phase ^= 1;
-        ptx::tc_fence_after();
         // visible keys of this row in block j: k <= lim (causal diagonal, ragged tail)
         int lim = kBM - 1;
         if (kCausal && j == i) lim = row;
         if (j == p.nblk - 1) lim = min(lim, p.N - 1 - j * kBM);
         if (!valid) lim = -1;
-#pragma unroll 1
-        for (int cc = 0; cc < kBM; cc += 32) {
-          uint32_t sr_[32], dp[32];
-          ptx::tmem_ld32(trow + kColS + cc, sr_);
-          ptx::tmem_ld32(trow + kColDP + cc, dp);
+        float pv[64];
+        ptx::mbar_wait(&ctrl->s_ready, s_phase);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int cc = 0; cc < 64; cc += 32) {
+          uint32_t sr_[32];
+          ptx::tmem_ld32(trow + kColS + k0c + cc, sr_);
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            const float pe = ptx::ex2(fmaf(__uint_as_float(sr_[k]), c, -lse2));
+            pv[cc + k] = (k0c + cc + k <= lim) ? pe : 0.f;
+          }
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&ctrl->p_ready);
+        ptx::mbar_wait(&ctrl->dp_ready, s_phase);
+        s_phase ^= 1;
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int cc = 0; cc < 64; cc += 32) {
+          uint32_t dp[32];
+          ptx::tmem_ld32(trow + kColDP + k0c + cc, dp);
           uint32_t pk[16];
 #pragma unroll
-          for (int k = 0; k < 32; k += 2) {
-            float p0 = ptx::ex2(fmaf(__uint_as_float(sr_[k]), c, -lse2));
-            float p1 = ptx::ex2(fmaf(__uint_as_float(sr_[k + 1]), c, -lse2));
-            p0 = (cc + k <= lim) ? p0 : 0.f;
-            p1 = (cc + k + 1 <= lim) ? p1 : 0.f;
-            const float ds0 = p0 * (__uint_as_float(dp[k]) - dd);
-            const float ds1 = p1 * (__uint_as_float(dp[k + 1]) - dd);
-            pk[k >> 1] = ptx::pack_bf16(ds0, ds1);
-          }
-          ptx::tmem_st16(trow + kColS + cc / 2, pk);  // dS (bf16 pairs) over S columns already consumed
+          for (int k = 0; k < 32; k += 2)
+            pk[k >> 1] = ptx::pack_bf16(pv[cc + k] * (__uint_as_float(dp[k]) - dd),
+                                        pv[cc + k + 1] * (__uint_as_float(dp[k + 1]) - dd));
+          ptx::tmem_st16(trow + kColDP + k0c + cc / 2, pk);  // dS (bf16 pairs) over dP columns this half read
         }
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&ctrl->p_ready);
+        if (lane == 0) ptx::mbar_arrive(&ctrl->ds_ready);
       }
       ptx::mbar_wait(&ctrl->o_ready, o_phase);
       o_phase ^= 1;
       ptx::tc_fence_after();
       __nv_bfloat16* dst = p.dq + ((long long)(b * p.Hq + h) * p.N + (valid ? qrow : 0)) * p.d_real;
 #pragma unroll
-      for (int cc = 0; cc < D; cc += 32) {
+      for (int cc = half * (D / 2); cc < (half + 1) * (D / 2); cc += 32) {  // each half stores D/2 columns
         uint32_t o[32];
         ptx::tmem_ld32(trow + kColDQ + cc, o);
         uint32_t pk[16];
@@ -374,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // ======================================================================== dK, dV
 template <int D, bool kCausal>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreadsKV, 1)
     attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                          const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                          const BwdParams p) {
@@ -387,11 +420,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // TMEM: S^T [0,128), dP^T [128,256), dV [256, 256+D), dK [384, 384+D)
   constexpr uint32_t kColS = 0, kColDP = 128, kColDV = 256, kColDK = 384;
+  constexpr int kEw = 8;  // elementwise warps
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kSchedRing; ++i) {
       ptx::mbar_init(&ctrl->sched_full[i], 1);
-      ptx::mbar_init(&ctrl->sched_empty[i], 2 + 4);
+      ptx::mbar_init(&ctrl->sched_empty[i], 2 + kEw);
     }
     ptx::mbar_init(&ctrl->a_full, 1);
     ptx::mbar_init(&ctrl->a_empty, 1);
@@ -400,7 +434,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(&ctrl->ring_empty[i], 1);
     }
     ptx::mbar_init(&ctrl->s_ready, 1);
-    ptx::mbar_init(&ctrl->p_ready, 4);
+    ptx::mbar_init(&ctrl->dp_ready, 1);
+    ptx::mbar_init(&ctrl->p_ready, kEw);
+    ptx::mbar_init(&ctrl->ds_ready, kEw);
     ptx::mbar_init(&ctrl->o_ready, 1);
     ptx::fence_barrier_init();
   }
@@ -451,6 +487,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
+    // Per block `it` the tensor pipe runs  dV(it) . S^T(it+1) . dK(it) . dP^T(it+1):
+    // the elementwise warps turn S^T(it+1) into P^T while dK(it) and dP^T(it+1)
+    // run, and dP^T(it+1) into dS^T while dV(it+1) and S^T(it+2) run.  (P^T
+    // aliases S^T and dS^T aliases dP^T, so each overwrite follows the MMA that
+    // reads the previous block's operand -- same-thread MMAs run in order.)
     BSchedReader sr;
     constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(kBM, kBM, 0, 0);  // S^T, dP^T
     constexpr uint32_t idesc_g = ptx::idesc_bf16_f32(kBM, D, 0, 1);    // dV, dK: A in TMEM, B MN-major
@@ -466,6 +507,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::mma_ss(tmem + d_col, a + off, b + off, idesc_s, k > 0 ? 1u : 0u);
       }
     };
+    // A operand (P^T or dS^T, bf16): queries 0-63 packed in columns [0,32) of
+    // the region, queries 64-127 in [64,96) -- each column half of the
+    // elementwise warps overwrites only the fp32 columns it has itself read.
+    auto ts_mma = [&](uint32_t d_col, uint32_t a_col, uint64_t b, bool acc0) {
+#pragma unroll
+      for (int k = 0; k < kBM / 16; ++k)
+        ptx::mma_ts(tmem + d_col, tmem + a_col + k * 8 + (k >= 4 ? 32 : 0), b + (uint64_t)((k * 16 * 128) >> 4), idesc_g,
+                    (acc0 || k > 0) ? 1u : 0u);
+    };
     while (true) {
       const int4 e = sr.next(ctrl);
       if (!e.w) break;
@@ -478,39 +528,45 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (ptx::elect_one_sync()) {
         const uint64_t qd = dr0 + (uint64_t)((st * 2 * C::kTile) >> 4);
         ss_mma(kColS, dkv0, qd);                                                            // S^T  = K Q_i^T
-        ss_mma(kColDP, dkv0 + (uint64_t)(C::kTile >> 4), qd + (uint64_t)(C::kTile >> 4));   // dP^T = V dO_i^T
         ptx::mma_commit(&ctrl->s_ready);
+        ss_mma(kColDP, dkv0 + (uint64_t)(C::kTile >> 4), qd + (uint64_t)(C::kTile >> 4));   // dP^T = V dO_i^T
+        ptx::mma_commit(&ctrl->dp_ready);
       }
       __syncwarp();
       for (int it = 0; it < n; ++it) {
-        ptx::mbar_wait(&ctrl->p_ready, p_phase);
-        p_phase ^= 1;
-        ptx::tc_fence_after();
         const int cur = st;
         const bool nxt = it + 1 < n;
         int nst = cur, nph = r_phase;
         if (nxt) {
           nst = cur + 1 == C::kStages ? 0 : cur + 1;
           nph = cur + 1 == C::kStages ? r_phase ^ 1 : r_phase;
+        }
+        const uint64_t qm = drm0 + (uint64_t)((cur * 2 * C::kTile) >> 4);  // Q_i as [queries x D] MN-major
+        const uint64_t dom = qm + (uint64_t)(C::kTile >> 4);               // dO_i likewise
+        const uint64_t qd = dr0 + (uint64_t)((nst * 2 * C::kTile) >> 4);
+        ptx::mbar_wait(&ctrl->p_ready, p_phase);
+        ptx::tc_fence_after();
+        if (nxt) {
           ptx::mbar_wait(&ctrl->ring_full[nst], nph);
           ptx::tc_fence_after();
         }
         if (ptx::elect_one_sync()) {
-          const uint64_t qm = drm0 + (uint64_t)((cur * 2 * C::kTile) >> 4);  // Q_i as [queries x D] MN-major
-          const uint64_t dom = qm + (uint64_t)(C::kTile >> 4);               // dO_i likewise
-#pragma unroll
-          for (int k = 0; k < kBM / 16; ++k) {
-            ptx::mma_ts(tmem + kColDV, tmem + kColS + k * 8, dom + (uint64_t)((k * 16 * 128) >> 4), idesc_g,
-                        (it > 0 || k > 0) ? 1u : 0u);   // dV += P^T dO_i
-            ptx::mma_ts(tmem + kColDK, tmem + kColDP + k * 8, qm + (uint64_t)((k * 16 * 128) >> 4), idesc_g,
-                        (it > 0 || k > 0) ? 1u : 0u);   // dK += dS^T Q_i
+          ts_mma(kColDV, kColS, dom, it > 0);                // dV += P^T dO_i
+          if (nxt) {
+            ss_mma(kColS, dkv0, qd);                         // S^T(it+1)
+            ptx::mma_commit(&ctrl->s_ready);
           }
+        }
+        __syncwarp();
+        ptx::mbar_wait(&ctrl->ds_ready, p_phase);
+        p_phase ^= 1;
+        ptx::tc_fence_after();
+        if (ptx::elect_one_sync()) {
+          ts_mma(kColDK, kColDP, qm, it > 0);                // dK += dS^T Q_i
           ptx::mma_commit(&ctrl->ring_empty[cur]);
           if (nxt) {
-            const uint64_t qd = dr0 + (uint64_t)((nst * 2 * C::kTile) >> 4);
-            ss_mma(kColS, dkv0, qd);
-            ss_mma(kColDP, dkv0 + (uint64_t)(C::kTile >> 4), qd + (uint64_t)(C::kTile >> 4));
-            ptx::mma_commit(&ctrl->s_ready);
+            ss_mma(kColDP, dkv0 + (uint64_t)(C::kTile >> 4), qd + (uint64_t)(C::kTile >> 4));  // dP^T(it+1)
+            ptx::mma_commit(&ctrl->dp_ready);
           } else {
             ptx::mma_commit(&ctrl->a_empty);
             ptx::mma_commit(&ctrl->o_ready);
@@ -526,7 +582,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 2) {
     if (lane == 0) bwd_scheduler(p, ctrl, p.Hkv);
   } else if (warp >= 4) {
+    // 256 threads: TMEM lane = key row (warp & 3), column half `half` = queries
+    // [64*half, 64*half+64) of each block.  Phase A: P^T = exp2(S^T*c - lse2)
+    // kept in registers (fp32) and stored bf16 over S^T; phase B: dS^T =
+    // P^T o (dP^T - D) stored bf16 over dP^T.
     const int quarter = warp & 3, krow = quarter * 32 + lane;  // key row of the block
+    const int half = (warp - 4) >> 2, q0c = half * 64;
+    const int et = threadIdx.x - 128;                           // 0..255
     const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
     const float c = p.scale_log2;
     BSchedReader sr;
@@ -540,55 +602,72 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int i0 = dkdv_first_qblock<kCausal>(j);
       for (int hh = 0; hh < p.G; ++hh) {
         for (int i = i0; i < p.nblk; ++i) {
-          ptx::mbar_wait(&ctrl->s_ready, s_phase);
-          s_phase ^= 1;
-          ptx::tc_fence_after();
-          // lse (as log2) and D of this block's 128 queries, staged in SMEM by the
-          // 128 elementwise threads (double-buffered by block parity)
+          // lse (as log2) and D of this block's 128 queries, staged in SMEM
+          // (double-buffered by block parity)
           const long long vi = (long long)(b * p.Hq + g * p.G + hh) * p.N + i * kBM;
           float* sv = svec + (blk & 1) * 2 * kBM;
           {
-            const bool ok = i * kBM + krow < p.N;
-            sv[krow] = ok ? __ldg(p.lse + vi + krow) * 1.4426950408889634f : 0.f;
-            sv[kBM + krow] = ok ? __ldg(p.dvec + vi + krow) : 0.f;
-            ptx::named_bar_sync(1, 128);
+            const int qq = et & (kBM - 1);
+            const bool ok = i * kBM + qq < p.N;
+            if (et < kBM) sv[qq] = ok ? __ldg(p.lse + vi + qq) * 1.4426950408889634f : 0.f;
+            else sv[kBM + qq] = ok ? __ldg(p.dvec + vi + qq) : 0.f;
+            ptx::named_bar_sync(1, 256);
           }
           ++blk;
-          // visible queries of this key: q >= k (causal), q < N; local query index qq
+          // visible queries of this key: q >= k (causal), q < N; local query index
           int qlo = 0, qhi = kBM - 1;
           if (kCausal && i == j) qlo = krow;           // query >= key
           if (i == p.nblk - 1) qhi = p.N - 1 - i * kBM;  // ragged tail
-#pragma unroll 1
-          for (int cc = 0; cc < kBM; cc += 32) {
-            uint32_t sr_[32], dp[32];
-            ptx::tmem_ld32(trow + kColS + cc, sr_);
-            ptx::tmem_ld32(trow + kColDP + cc, dp);
-            uint32_t pp[16], pd[16];
+          float pv[64];
+          ptx::mbar_wait(&ctrl->s_ready, s_phase);
+          ptx::tc_fence_after();
+#pragma unroll
+          for (int cc = 0; cc < 64; cc += 32) {
+            uint32_t sr_[32];
+            ptx::tmem_ld32(trow + kColS + q0c + cc, sr_);
+            uint32_t pp[16];
 #pragma unroll
             for (int k = 0; k < 32; k += 4) {
-              const float4 l4 = *reinterpret_cast<const float4*>(sv + cc + k);
-              const float4 d4 = *reinterpret_cast<const float4*>(sv + kBM + cc + k);
-              const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dvv[4] = {d4.x, d4.y, d4.z, d4.w};
+              const float4 l4 = *reinterpret_cast<const float4*>(sv + q0c + cc + k);
+              const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
 #pragma unroll
-              for (int u = 0; u < 4; u += 2) {
-                const int q0 = cc + k + u, q1 = q0 + 1;
-                const bool v0 = q0 >= qlo && q0 <= qhi, v1 = q1 >= qlo && q1 <= qhi;
-                float p0 = ptx::ex2(fmaf(__uint_as_float(sr_[k + u]), c, -lv[u]));
-                float p1 = ptx::ex2(fmaf(__uint_as_float(sr_[k + u + 1]), c, -lv[u + 1]));
-                p0 = v0 ? p0 : 0.f;
-                p1 = v1 ? p1 : 0.f;
-                pp[(k + u) >> 1] = ptx::pack_bf16(p0, p1);
-                pd[(k + u) >> 1] = ptx::pack_bf16(p0 * (__uint_as_float(dp[k + u]) - dvv[u]),
-                                                  p1 * (__uint_as_float(dp[k + u + 1]) - dvv[u + 1]));
+              for (int u = 0; u < 4; ++u) {
+                const int q = q0c + cc + k + u;
+                const float pe = ptx::ex2(fmaf(__uint_as_float(sr_[k + u]), c, -lv[u]));
+                pv[cc + k + u] = (q >= qlo && q <= qhi) ? pe : 0.f;
               }
+#pragma unroll
+              for (int u = 0; u < 4; u += 2) pp[(k + u) >> 1] = ptx::pack_bf16(pv[cc + k + u], pv[cc + k + u + 1]);
             }
-            ptx::tmem_st16(trow + kColS + cc / 2, pp);   // P^T over consumed S^T columns
-            ptx::tmem_st16(trow + kColDP + cc / 2, pd);  // dS^T over consumed dP^T columns
+            ptx::tmem_st16(trow + kColS + q0c + cc / 2, pp);   // P^T over consumed S^T columns
           }
           ptx::tmem_wait_st();
           ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&ctrl->p_ready);
+          ptx::mbar_wait(&ctrl->dp_ready, s_phase);
+          s_phase ^= 1;
+          ptx::tc_fence_after();
+#pragma unroll
+          for (int cc = 0; cc < 64; cc += 32) {
+            uint32_t dp[32];
+            ptx::tmem_ld32(trow + kColDP + q0c + cc, dp);
+            uint32_t pd[16];
+#pragma unroll
+            for (int k = 0; k < 32; k += 4) {
+              const float4 d4 = *reinterpret_cast<const float4*>(sv + kBM + q0c + cc + k);
+              const float dvv[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+              for (int u = 0; u < 4; u += 2)
+                pd[(k + u) >> 1] = ptx::pack_bf16(pv[cc + k + u] * (__uint_as_float(dp[k + u]) - dvv[u]),
+                                                  pv[cc + k + u + 1] * (__uint_as_float(dp[k + u + 1]) - dvv[u + 1]));
+            }
+            ptx::tmem_st16(trow + kColDP + q0c + cc / 2, pd);  // dS^T over consumed dP^T columns
+          }
+          ptx::tmem_wait_st();
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&ctrl->ds_ready);
         }
       }
       ptx::mbar_wait(&ctrl->o_ready, o_phase);
@@ -596,8 +675,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::tc_fence_after();
       const bool valid = kglob < p.N;
       const long long ro = ((long long)(b * p.Hkv + g) * p.N + (valid ? kglob : 0)) * p.d_real;
-#pragma unroll
-      for (int which = 0; which < 2; ++which) {
+      {
+        const int which = half;  // column half 0 writes dV, half 1 writes dK
         __nv_bfloat16* dst = (which == 0 ? p.dv : p.dk) + ro;
         const float f = which == 0 ? 1.f : p.scale;
         const uint32_t col = which == 0 ? kColDV : kColDK;
