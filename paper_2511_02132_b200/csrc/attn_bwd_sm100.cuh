@@ -38,11 +38,17 @@ struct BCfg {
   static constexpr int kChunks = D / 64;
   static constexpr int kTile = kBM * D * 2;  // one 128 x D bf16 tile
   static constexpr int kStages = 2;          // ring depth of the streamed operand pairs
-  static constexpr int kOffA = 0;            // resident pair (dQ: Q, dO;  dKdV: K, V)
-  static constexpr int kOffRing = 2 * kTile;  // ring of streamed pairs (dQ: K, V;  dKdV: Q, dO)
-  static constexpr int kOffVec = kOffRing + kStages * 2 * kTile;  // dKdV: staged lse2 / D (2 parities)
-  static constexpr int kOffCtrl = kOffVec + kStages * 2 * kBM * 4;
-  static constexpr int kSmemBytes = kOffCtrl + 1024 + 1024;
+  // Control block and staged vectors first, then the 1024-B aligned tiles; the
+  // dynamic SMEM base is 1024-B aligned (checked in-kernel), which lets the
+  // dK/dV kernel use the full 227 KB at D = 128.
+  static constexpr int kOffCtrl = 0;          // BCtrl (<= 1 KB)
+  static constexpr int kOffVec = 1024;        // dKdV: staged lse2 / D (2 parities x 2 x 128 floats)
+  static constexpr int kOffA = 3072;          // resident pair (dQ: Q, dO;  dKdV: K, V)
+  static constexpr int kOffRing = kOffA + 2 * kTile;  // ring of streamed pairs (dQ: K, V;  dKdV: Q, dO)
+  static constexpr int kOffPT = kOffRing + kStages * 2 * kTile;  // dKdV: P^T, 128 x 128 bf16 (SW128 K-major)
+  static constexpr int kSmemBytes = kOffPT;                      // dQ kernel
+  static constexpr int kSmemBytesKV = kOffPT + kBM * kBM * 2;    // dK/dV kernel
+  static_assert(kSmemBytesKV <= 232448, "dK/dV SMEM over the 227 KB opt-in limit");
 };
 
 struct BwdParams {
@@ -66,10 +72,12 @@ struct __align__(16) BCtrl {
   uint64_t a_full, a_empty;             // resident pair
   uint64_t ring_full[4], ring_empty[4]; // streamed pairs
   uint64_t s_ready, p_ready, o_ready;
-  uint64_t dp_ready, ds_ready;          // dKdV: dP^T in TMEM, dS^T stored
+  uint64_t dp_ready, ds_ready;          // dP in TMEM, dS stored (bf16, TMEM)
+  uint64_t s_free, dv_done;             // dKdV: S^T read into registers; dV MMA done (P^T SMEM free)
   int4 entry[kSchedRing];
   uint32_t tmem_base;
 };
+static_assert(sizeof(BCtrl) <= 1024, "BCtrl must fit its 1 KB slot");
 
 // The scheduler warp: identical pop / steal / broadcast protocol as the forward.
 __device__ __forceinline__ void bwd_scheduler(const BwdParams& p, BCtrl* ctrl, int Hsched) {
@@ -157,8 +165,9 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
                        const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                        const BwdParams p) {
   using C = BCfg<D>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
+  if (ptx::smem_u32(smem_raw) & 1023) __trap();  // layout relies on a 1024-B aligned base
   uint8_t* sq = smem + C::kOffA;             // Q tile, then dO tile
   uint8_t* ring = smem + C::kOffRing;        // stage s: K at 2s, V at 2s+1
   BCtrl* ctrl = reinterpret_cast<BCtrl*>(smem + C::kOffCtrl);
@@ -412,10 +421,12 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
                          const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                          const BwdParams p) {
   using C = BCfg<D>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
+  if (ptx::smem_u32(smem_raw) & 1023) __trap();  // layout relies on a 1024-B aligned base
   uint8_t* skv = smem + C::kOffA;            // K tile, then V tile
   uint8_t* ring = smem + C::kOffRing;        // stage s: Q at 2s, dO at 2s+1
+  uint8_t* spt = smem + C::kOffPT;           // P^T (bf16) as the A operand of dV
   BCtrl* ctrl = reinterpret_cast<BCtrl*>(smem + C::kOffCtrl);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // TMEM: S^T [0,128), dP^T [128,256), dV [256, 256+D), dK [384, 384+D)
@@ -437,6 +448,8 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
     ptx::mbar_init(&ctrl->dp_ready, 1);
     ptx::mbar_init(&ctrl->p_ready, kEw);
     ptx::mbar_init(&ctrl->ds_ready, kEw);
+    ptx::mbar_init(&ctrl->s_free, kEw);
+    ptx::mbar_init(&ctrl->dv_done, 1);
     ptx::mbar_init(&ctrl->o_ready, 1);
     ptx::fence_barrier_init();
   }
@@ -487,17 +500,18 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
       }
     }
   } else if (warp == 1) {
-    // Per block `it` the tensor pipe runs  dV(it) . S^T(it+1) . dK(it) . dP^T(it+1):
-    // the elementwise warps turn S^T(it+1) into P^T while dK(it) and dP^T(it+1)
-    // run, and dP^T(it+1) into dS^T while dV(it+1) and S^T(it+2) run.  (P^T
-    // aliases S^T and dS^T aliases dP^T, so each overwrite follows the MMA that
-    // reads the previous block's operand -- same-thread MMAs run in order.)
+    // Per block `it` the tensor pipe runs  S^T(it+1) . dV(it) . dK(it) . dP^T(it+1):
+    // S^T(it+1) is issued as soon as the elementwise warps hold S^T(it) in
+    // registers (s_free), dV(it) once they have written P^T(it) to SMEM, dK(it)
+    // once dS^T(it) is in TMEM over dP^T(it) -- the exps of block it+1 overlap
+    // dV(it), dK(it) and dP^T(it+1).
     BSchedReader sr;
     constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(kBM, kBM, 0, 0);  // S^T, dP^T
-    constexpr uint32_t idesc_g = ptx::idesc_bf16_f32(kBM, D, 0, 1);    // dV, dK: A in TMEM, B MN-major
+    constexpr uint32_t idesc_g = ptx::idesc_bf16_f32(kBM, D, 0, 1);    // dV, dK: A K-major, B MN-major
     const uint64_t dkv0 = ptx::smem_desc_sw128(ptx::smem_u32(skv), 16, 1024);
     const uint64_t dr0 = ptx::smem_desc_sw128(ptx::smem_u32(ring), 16, 1024);
     const uint64_t drm0 = ptx::smem_desc_sw128(ptx::smem_u32(ring), kBM * 128, 1024);
+    const uint64_t dpt0 = ptx::smem_desc_sw128(ptx::smem_u32(spt), 16, 1024);
     uint32_t a_phase = 0, r_phase = 0, p_phase = 0;
     int stage = 0;
     auto ss_mma = [&](uint32_t d_col, uint64_t a, uint64_t b) {
@@ -506,15 +520,6 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
         const uint32_t off = ((k >> 2) * (kBM * 128) + (k & 3) * 32) >> 4;
         ptx::mma_ss(tmem + d_col, a + off, b + off, idesc_s, k > 0 ? 1u : 0u);
       }
-    };
-    // A operand (P^T or dS^T, bf16): queries 0-63 packed in columns [0,32) of
-    // the region, queries 64-127 in [64,96) -- each column half of the
-    // elementwise warps overwrites only the fp32 columns it has itself read.
-    auto ts_mma = [&](uint32_t d_col, uint32_t a_col, uint64_t b, bool acc0) {
-#pragma unroll
-      for (int k = 0; k < kBM / 16; ++k)
-        ptx::mma_ts(tmem + d_col, tmem + a_col + k * 8 + (k >= 4 ? 32 : 0), b + (uint64_t)((k * 16 * 128) >> 4), idesc_g,
-                    (acc0 || k > 0) ? 1u : 0u);
     };
     while (true) {
       const int4 e = sr.next(ctrl);
@@ -544,25 +549,38 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
         const uint64_t qm = drm0 + (uint64_t)((cur * 2 * C::kTile) >> 4);  // Q_i as [queries x D] MN-major
         const uint64_t dom = qm + (uint64_t)(C::kTile >> 4);               // dO_i likewise
         const uint64_t qd = dr0 + (uint64_t)((nst * 2 * C::kTile) >> 4);
-        ptx::mbar_wait(&ctrl->p_ready, p_phase);
+        ptx::mbar_wait(&ctrl->s_free, p_phase);
         ptx::tc_fence_after();
         if (nxt) {
           ptx::mbar_wait(&ctrl->ring_full[nst], nph);
           ptx::tc_fence_after();
-        }
-        if (ptx::elect_one_sync()) {
-          ts_mma(kColDV, kColS, dom, it > 0);                // dV += P^T dO_i
-          if (nxt) {
+          if (ptx::elect_one_sync()) {
             ss_mma(kColS, dkv0, qd);                         // S^T(it+1)
             ptx::mma_commit(&ctrl->s_ready);
           }
+          __syncwarp();
+        }
+        ptx::mbar_wait(&ctrl->p_ready, p_phase);
+        ptx::tc_fence_after();
+        if (ptx::elect_one_sync()) {
+#pragma unroll
+          for (int k = 0; k < kBM / 16; ++k)                // dV += P^T dO_i  (A = P^T from SMEM)
+            ptx::mma_ss(tmem + kColDV, dpt0 + (uint64_t)((((k >> 2) * (kBM * 128)) + (k & 3) * 32) >> 4),
+                        dom + (uint64_t)((k * 16 * 128) >> 4), idesc_g, (it > 0 || k > 0) ? 1u : 0u);
+          ptx::mma_commit(&ctrl->dv_done);
         }
         __syncwarp();
         ptx::mbar_wait(&ctrl->ds_ready, p_phase);
         p_phase ^= 1;
         ptx::tc_fence_after();
         if (ptx::elect_one_sync()) {
-          ts_mma(kColDK, kColDP, qm, it > 0);                // dK += dS^T Q_i
+          // dK += dS^T Q_i: A = dS^T (bf16 in TMEM over dP^T; queries 0-63 packed
+          // in columns [0,32) of the region, 64-127 in [64,96) -- each column half
+          // of the elementwise warps overwrites only columns it has itself read)
+#pragma unroll
+          for (int k = 0; k < kBM / 16; ++k)
+            ptx::mma_ts(tmem + kColDK, tmem + kColDP + k * 8 + (k >= 4 ? 32 : 0),
+                        qm + (uint64_t)((k * 16 * 128) >> 4), idesc_g, (it > 0 || k > 0) ? 1u : 0u);
           ptx::mma_commit(&ctrl->ring_empty[cur]);
           if (nxt) {
             ss_mma(kColDP, dkv0 + (uint64_t)(C::kTile >> 4), qd + (uint64_t)(C::kTile >> 4));  // dP^T(it+1)
@@ -584,15 +602,15 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
   } else if (warp >= 4) {
     // 256 threads: TMEM lane = key row (warp & 3), column half `half` = queries
     // [64*half, 64*half+64) of each block.  Phase A: P^T = exp2(S^T*c - lse2)
-    // kept in registers (fp32) and stored bf16 over S^T; phase B: dS^T =
-    // P^T o (dP^T - D) stored bf16 over dP^T.
+    // kept in registers (fp32) and stored bf16 to SMEM for the dV MMA; phase B:
+    // dS^T = P^T o (dP^T - D) stored bf16 over dP^T.
     const int quarter = warp & 3, krow = quarter * 32 + lane;  // key row of the block
     const int half = (warp - 4) >> 2, q0c = half * 64;
     const int et = threadIdx.x - 128;                           // 0..255
     const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
     const float c = p.scale_log2;
     BSchedReader sr;
-    uint32_t s_phase = 0, o_phase = 0, blk = 0;
+    uint32_t s_phase = 0, o_phase = 0, blk = 0, pt_phase = 0;
     float* svec = reinterpret_cast<float*>(smem + C::kOffVec);  // [parity][lse2 | D]
     while (true) {
       const int4 e = sr.next(ctrl);
@@ -621,28 +639,35 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
           float pv[64];
           ptx::mbar_wait(&ctrl->s_ready, s_phase);
           ptx::tc_fence_after();
-#pragma unroll
-          for (int cc = 0; cc < 64; cc += 32) {
-            uint32_t sr_[32];
-            ptx::tmem_ld32(trow + kColS + q0c + cc, sr_);
-            uint32_t pp[16];
-#pragma unroll
-            for (int k = 0; k < 32; k += 4) {
-              const float4 l4 = *reinterpret_cast<const float4*>(sv + q0c + cc + k);
-              const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                const int q = q0c + cc + k + u;
-                const float pe = ptx::ex2(fmaf(__uint_as_float(sr_[k + u]), c, -lv[u]));
-                pv[cc + k + u] = (q >= qlo && q <= qhi) ? pe : 0.f;
-              }
-#pragma unroll
-              for (int u = 0; u < 4; u += 2) pp[(k + u) >> 1] = ptx::pack_bf16(pv[cc + k + u], pv[cc + k + u + 1]);
-            }
-            ptx::tmem_st16(trow + kColS + q0c + cc / 2, pp);   // P^T over consumed S^T columns
-          }
-          ptx::tmem_wait_st();
+          ptx::tmem_ld32(trow + kColS + q0c, reinterpret_cast<uint32_t*>(pv));
+          ptx::tmem_ld32(trow + kColS + q0c + 32, reinterpret_cast<uint32_t*>(pv) + 32);
           ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&ctrl->s_free);   // S^T region may be overwritten
+#pragma unroll
+          for (int k = 0; k < 64; k += 4) {
+            const float4 l4 = *reinterpret_cast<const float4*>(sv + q0c + k);
+            const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int q = q0c + k + u;
+              const float pe = ptx::ex2(fmaf(pv[k + u], c, -lv[u]));
+              pv[k + u] = (q >= qlo && q <= qhi) ? pe : 0.f;
+            }
+          }
+          // P^T -> SMEM (SW128 K-major: key row krow, 16-B unit u at (u ^ (krow & 7)))
+          // once dV of the previous block has read the buffer
+          ptx::mbar_wait(&ctrl->dv_done, pt_phase ^ 1);
+          pt_phase ^= 1;
+          {
+            uint8_t* rowp = spt + half * (kBM * 128) + krow * 128;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              *reinterpret_cast<uint4*>(rowp + ((u ^ (krow & 7)) << 4)) =
+                  make_uint4(ptx::pack_bf16(pv[8 * u + 0], pv[8 * u + 1]), ptx::pack_bf16(pv[8 * u + 2], pv[8 * u + 3]),
+                             ptx::pack_bf16(pv[8 * u + 4], pv[8 * u + 5]), ptx::pack_bf16(pv[8 * u + 6], pv[8 * u + 7]));
+          }
+          ptx::fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&ctrl->p_ready);
           ptx::mbar_wait(&ctrl->dp_ready, s_phase);
