@@ -9,8 +9,9 @@
 // workgroup computing different row blocks of the gradients ... may share the
 // same Q, K, V, and dO tensors within the same attention head"):
 //   attn_bwd_dot_kernel   D[b,h,i] = sum_c dO * O                (bandwidth)
-//   attn_bwd_dq_kernel    unit = (b, h, 128-row query block); loops over key
-//                         blocks: S = Q K_j^T and dP = dO V_j^T (SS MMAs) ->
+//   attn_bwd_dq_kernel    unit = (b, h, 128-row query block); Q and dO copied
+//                         to TMEM once per unit; loops over key blocks:
+//                         S = Q K_j^T and dP = dO V_j^T (TS MMAs) ->
 //                         P (registers), dS (8 elementwise warps: TMEM lane =
 //                         query row, two key halves; bf16 into TMEM over dP)
 //                         -> dQ += dS K_j (TS MMA).
@@ -73,6 +74,7 @@ struct __align__(16) BCtrl {
   uint64_t ring_full[4], ring_empty[4]; // streamed pairs
   uint64_t s_ready, p_ready, o_ready;
   uint64_t dp_ready, ds_ready;          // dP in TMEM, dS stored (bf16, TMEM)
+  uint64_t q_ready;                     // dQ: Q and dO copied into TMEM
   uint64_t s_free, dv_done;             // dKdV: S^T read into registers; dV MMA done (P^T SMEM free)
   int4 entry[kSchedRing];
   uint32_t tmem_base;
@@ -172,8 +174,10 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
   uint8_t* ring = smem + C::kOffRing;        // stage s: K at 2s, V at 2s+1
   BCtrl* ctrl = reinterpret_cast<BCtrl*>(smem + C::kOffCtrl);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // TMEM: S [0,128), dP [128,256), dQ [256, 256+D)
-  constexpr uint32_t kColS = 0, kColDP = 128, kColDQ = 256;
+  // TMEM: S [0,128), dP [128,256), dQ [256, 256+D), Q [384, 384+D/2), dO [448, 448+D/2)
+  // (Q and dO as bf16 pairs: the A operands of the S and dP MMAs come from TMEM,
+  // so those MMAs read only K / V from SMEM)
+  constexpr uint32_t kColS = 0, kColDP = 128, kColDQ = 256, kColQ = 384, kColDO = 448;
   constexpr int kEw = 8;  // elementwise warps
 
   if (threadIdx.x == 0) {
@@ -182,11 +186,12 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
       ptx::mbar_init(&ctrl->sched_empty[i], 2 + kEw);
     }
     ptx::mbar_init(&ctrl->a_full, 1);
-    ptx::mbar_init(&ctrl->a_empty, 1);
+    ptx::mbar_init(&ctrl->a_empty, kEw);   // Q / dO SMEM copied into TMEM
     for (int i = 0; i < C::kStages; ++i) {
       ptx::mbar_init(&ctrl->ring_full[i], 1);
       ptx::mbar_init(&ctrl->ring_empty[i], 1);
     }
+    ptx::mbar_init(&ctrl->q_ready, kEw);
     ptx::mbar_init(&ctrl->s_ready, 1);
     ptx::mbar_init(&ctrl->dp_ready, 1);
     ptx::mbar_init(&ctrl->p_ready, kEw);   // S consumed (P held in registers)
@@ -245,32 +250,31 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
     BSchedReader sr;
     constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(kBM, kBM, 0, 0);  // S, dP: K-major A and B
     constexpr uint32_t idesc_q = ptx::idesc_bf16_f32(kBM, D, 0, 1);    // dQ: A = dS (TMEM), B = K MN-major
-    const uint64_t da0 = ptx::smem_desc_sw128(ptx::smem_u32(sq), 16, 1024);
     const uint64_t dr0 = ptx::smem_desc_sw128(ptx::smem_u32(ring), 16, 1024);
     const uint64_t drm0 = ptx::smem_desc_sw128(ptx::smem_u32(ring), kBM * 128, 1024);
     uint32_t a_phase = 0, r_phase = 0, p_phase = 0;
     int stage = 0;
-    auto ss_mma = [&](uint32_t d_col, uint64_t a, uint64_t b) {  // [128 x 128] = A[128 x D] B[128 x D]^T
+    auto ts_mma = [&](uint32_t d_col, uint32_t a_col, uint64_t b) {  // [128 x 128] = A[128 x D] (TMEM) B[128 x D]^T
 #pragma unroll
       for (int k = 0; k < D / 16; ++k) {
         const uint32_t off = ((k >> 2) * (kBM * 128) + (k & 3) * 32) >> 4;
-        ptx::mma_ss(tmem + d_col, a + off, b + off, idesc_s, k > 0 ? 1u : 0u);
+        ptx::mma_ts(tmem + d_col, tmem + a_col + k * 8, b + off, idesc_s, k > 0 ? 1u : 0u);
       }
     };
     while (true) {
       const int4 e = sr.next(ctrl);
       if (!e.w) break;
       const int n = dq_nblocks<kCausal>(e.z, p.nblk);
-      ptx::mbar_wait(&ctrl->a_full, a_phase);
+      ptx::mbar_wait(&ctrl->q_ready, a_phase);
       a_phase ^= 1;
       int st = stage;
       ptx::mbar_wait(&ctrl->ring_full[st], r_phase);
       ptx::tc_fence_after();
       if (ptx::elect_one_sync()) {
         const uint64_t kd = dr0 + (uint64_t)((st * 2 * C::kTile) >> 4);
-        ss_mma(kColS, da0, kd);                                                 // S  = Q  K_0^T
+        ts_mma(kColS, kColQ, kd);                                   // S  = Q  K_0^T
         ptx::mma_commit(&ctrl->s_ready);
-        ss_mma(kColDP, da0 + (uint64_t)(C::kTile >> 4), kd + (uint64_t)(C::kTile >> 4));  // dP = dO V_0^T
+        ts_mma(kColDP, kColDO, kd + (uint64_t)(C::kTile >> 4));     // dP = dO V_0^T
         ptx::mma_commit(&ctrl->dp_ready);
       }
       __syncwarp();
@@ -289,7 +293,7 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
           ptx::mbar_wait(&ctrl->ring_full[nst], nph);
           ptx::tc_fence_after();
           if (ptx::elect_one_sync()) {
-            ss_mma(kColS, da0, kd);                 // S(j+1)
+            ts_mma(kColS, kColQ, kd);               // S(j+1)
             ptx::mma_commit(&ctrl->s_ready);
           }
           __syncwarp();
@@ -308,10 +312,9 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
                         km + (uint64_t)((k * 16 * 128) >> 4), idesc_q, (j > 0 || k > 0) ? 1u : 0u);
           ptx::mma_commit(&ctrl->ring_empty[cur]);
           if (nxt) {
-            ss_mma(kColDP, da0 + (uint64_t)(C::kTile >> 4), kd + (uint64_t)(C::kTile >> 4));  // dP(j+1)
+            ts_mma(kColDP, kColDO, kd + (uint64_t)(C::kTile >> 4));  // dP(j+1)
             ptx::mma_commit(&ctrl->dp_ready);
           } else {
-            ptx::mma_commit(&ctrl->a_empty);
             ptx::mma_commit(&ctrl->o_ready);
           }
         }
@@ -332,11 +335,36 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
     const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
     const float c = p.scale_log2;
     BSchedReader sr;
-    uint32_t s_phase = 0, o_phase = 0;
+    uint32_t s_phase = 0, o_phase = 0, a_phase = 0;
     while (true) {
       const int4 e = sr.next(ctrl);
       if (!e.w) break;
       const int b = e.x, h = e.y, i = e.z;
+      {
+        // Q, dO (SW128 K-major SMEM, 64-column chunks) -> TMEM as bf16 pairs;
+        // column half `half` copies chunks half, half + 2, ...
+        ptx::mbar_wait(&ctrl->a_full, a_phase);
+        a_phase ^= 1;
+#pragma unroll
+        for (int ch = half; ch < 2 * C::kChunks; ch += 2) {
+          const int t = ch / C::kChunks, cc = ch % C::kChunks;
+          const uint8_t* rowp = sq + t * C::kTile + cc * (kBM * 128) + row * 128;
+          uint32_t v[32];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const uint4 x = *reinterpret_cast<const uint4*>(rowp + ((u ^ (row & 7)) << 4));
+            v[4 * u] = x.x; v[4 * u + 1] = x.y; v[4 * u + 2] = x.z; v[4 * u + 3] = x.w;
+          }
+          ptx::tmem_st32(trow + (t ? kColDO : kColQ) + cc * 32, v);
+        }
+        ptx::tmem_wait_st();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          ptx::mbar_arrive(&ctrl->q_ready);
+          ptx::mbar_arrive(&ctrl->a_empty);
+        }
+      }
       const int qrow = i * kBM + row;
       const bool valid = qrow < p.N;
       const long long ridx = (long long)(b * p.Hq + h) * p.N + (valid ? qrow : 0);
