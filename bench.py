@@ -220,21 +220,45 @@ def run_ours(a):
         by_mapping[m] = {"tflops": round(flops_job / (msm * 1e-3) / 1e12, 1), "ms_per_step": round(msm, 4),
                          "l2_hit_rate_pct": prof.get("lts__t_sector_hit_rate.pct") if prof else None}
 
-    # end to end through the public API on pinned host buffers (forward)
-    qh, kh, vh, _ = sets[0]
-    qh, kh, vh = (t.cpu().pin_memory() for t in (qh, kh, vh))
-    oh = torch.empty_like(qh).pin_memory()
+    # end to end through the public API on pinned host buffers
     e2e_steps = max(2, min(a.steps, 10))
+    if a.pass_ == "fwd":
+        qh, kh, vh, _ = sets[0]
+        qh, kh, vh = (t.cpu().pin_memory() for t in (qh, kh, vh))
+        oh = torch.empty_like(qh).pin_memory()
+
+        def e2e_step():
+            api.attn_fwd_host(qh, kh, vh, oh, causal=causal, scale=scale, mapping=a.mapping, stream=stream)
+        h2d = sum(t.numel() * t.element_size() for t in (qh, kh, vh))
+        d2h = oh.numel() * oh.element_size()
+        e2e_api = "attn_fwd_host (pinned host buffers, H2D + kernel + D2H + sync)"
+    else:
+        # q, k, v, O, dO, lse host -> device; attn_bwd; dq, dk, dv device -> host
+        ins_h = [t.cpu().pin_memory() for t in (*sets[0][:3], *bwd_inputs[0])]
+        ins_d = [torch.empty_like(t, device=dev) for t in ins_h]
+        outs_d = [torch.empty_like(ins_d[i]) for i in range(3)]
+        outs_h = [torch.empty_like(ins_h[i]).pin_memory() for i in range(3)]
+
+        def e2e_step():
+            for hsrc, ddst in zip(ins_h, ins_d):
+                ddst.copy_(hsrc, non_blocking=True)
+            qd, kd, vd, od, lsed, dod = ins_d
+            api.attn_bwd(qd, kd, vd, od, dod, lsed, causal=causal, scale=scale, mapping=a.mapping,
+                         dq=outs_d[0], dk=outs_d[1], dv=outs_d[2], stream=stream)
+            for dsrc, hdst in zip(outs_d, outs_h):
+                hdst.copy_(dsrc, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        h2d = sum(t.numel() * t.element_size() for t in ins_h)
+        d2h = sum(t.numel() * t.element_size() for t in outs_h)
+        e2e_api = "attn_bwd (pinned host q,k,v,O,dO,lse -> H2D + kernels + D2H of dq,dk,dv + sync)"
     for _ in range(2):
-        api.attn_fwd_host(qh, kh, vh, oh, causal=causal, scale=scale, mapping=a.mapping, stream=stream)
+        e2e_step()
     if world > 1:
         torch.distributed.barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        api.attn_fwd_host(qh, kh, vh, oh, causal=causal, scale=scale, mapping=a.mapping, stream=stream)
+        e2e_step()
     t_e2e = pdist.max_over_ranks((time.perf_counter() - t0) / e2e_steps, dev)
-    h2d = sum(t.numel() * t.element_size() for t in (qh, kh, vh))
-    d2h = oh.numel() * oh.element_size()
 
     peak, peak_sus, peak_src = load_peaks()
     achieved = flops_rank / (ms_kernel * 1e-3) / 1e12
@@ -250,7 +274,8 @@ def run_ours(a):
         "config": {"workload": a.workload, "B": B, "Hq": Hq_job, "Hkv": Hkv_job, "N": N, "d": d, "causal": causal,
                    "mapping": a.mapping, "pass": a.pass_, "heads_per_gpu": hq,
                    "parallelism": f"heads sharded over {world} GPU(s), no data-path collective",
-                   "l2": l2_note, "flop_convention": "4*B*Hq*N^2*d, causal x0.5"},
+                   "l2": l2_note, "flop_convention": ("4*B*Hq*N^2*d, causal x0.5" if a.pass_ == "fwd" else
+                                                      "10*B*Hq*N^2*d (5 matmuls), causal x0.5")},
         "roofline": {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
                      "peak_source": f"bf16_tflops {peak_src} (burst: one kernel per step)",
@@ -261,7 +286,7 @@ def run_ours(a):
                      "lat_far_cyc": round(topo["lat_far_cyc"], 1)},
         "e2e": {"value": round(flops_job / t_e2e / 1e12, 2), "unit": "TFLOP/s", "h2d_bytes_per_step": h2d * world,
                 "d2h_bytes_per_step": d2h * world, "ms_per_step": round(t_e2e * 1e3, 3),
-                "api": "attn_fwd_host (pinned host buffers, H2D + kernel + D2H + sync)"},
+                "api": e2e_api},
         "gpu_launches": launches,
         "clocks": clocks,
     }

@@ -100,15 +100,22 @@ def attn_fwd_lse(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: b
 
 def attn_bwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor, dout: torch.Tensor,
              lse: torch.Tensor, *, causal: bool = False, scale: Optional[float] = None,
-             mapping="swizzled_head_first", order: str = "ascending", stream: Optional[torch.cuda.Stream] = None):
-    """Gradients (dq, dk, dv) of sum(dout * attention(q, k, v)) (PAPER.md eq:ba), bf16."""
+             mapping="swizzled_head_first", order: str = "ascending", stream: Optional[torch.cuda.Stream] = None,
+             dq: Optional[torch.Tensor] = None, dk: Optional[torch.Tensor] = None, dv: Optional[torch.Tensor] = None):
+    """Gradients (dq, dk, dv) of sum(dout * attention(q, k, v)) (PAPER.md eq:ba), bf16.
+    dq / dk / dv may be passed as preallocated outputs (shaped like q / k / v)."""
     for name, t in (("q", q), ("k", k), ("v", v), ("o", o), ("dout", dout)):
         if t.dtype != torch.bfloat16 or not t.is_cuda or not t.is_contiguous():
             raise TypeError(f"{name} must be a contiguous bfloat16 CUDA tensor")
-    if lse.dtype != torch.float32 or not lse.is_contiguous():
+    if lse.dtype != torch.float32 or not lse.is_cuda or not lse.is_contiguous():
         raise TypeError("lse must be a contiguous float32 CUDA tensor")
     B, Hq, N, d = q.shape
-    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    dq = torch.empty_like(q) if dq is None else dq
+    dk = torch.empty_like(k) if dk is None else dk
+    dv = torch.empty_like(v) if dv is None else dv
+    for name, t, ref in (("dq", dq, q), ("dk", dk, k), ("dv", dv, v)):
+        if t.shape != ref.shape or t.dtype != torch.bfloat16 or not t.is_cuda or not t.is_contiguous():
+            raise TypeError(f"{name} must be a contiguous bfloat16 CUDA tensor shaped like {name[1:]}")
     if scale is None:
         scale = 1.0 / math.sqrt(d)
     lib = _lib.load()
