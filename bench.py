@@ -63,9 +63,9 @@ def load_peaks():
         return 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
 
 
-def load_profile_summary(workload, mapping):
+def load_profile_summary(workload, mapping, cluster=False):
     """ncu --set full summary committed under profiles/ for this workload/mapping, if any."""
-    path = os.path.join(ROOT, "profiles", f"ncu_{workload}_{mapping}.json")
+    path = os.path.join(ROOT, "profiles", f"ncu_{workload}_{mapping}{'_cluster' if cluster else ''}.json")
     try:
         with open(path) as f:
             return json.load(f)
@@ -173,7 +173,10 @@ def run_ours(a):
             o2, lse, do = bwd_inputs[i % n_sets]
             api.attn_bwd(q, k, v, o2, do, lse, causal=causal, scale=scale, mapping=mapping, stream=stream)
         else:
-            api.attn_fwd(q, k, v, o, causal=causal, scale=scale, mapping=mapping, stream=stream)
+            api.attn_fwd(q, k, v, o, causal=causal, scale=scale, mapping=mapping, stream=stream,
+                         cluster=bool(cluster_on[0]))
+
+    cluster_on = [a.cluster if a.pass_ == "fwd" else 0]
 
     def timed(mapping, steps, warmup, sampler=None):
         for i in range(warmup):
@@ -209,16 +212,28 @@ def run_ours(a):
     clocks = sampler.summary()
     value = flops_job / (ms_step * 1e-3) / 1e12
 
-    # the same workload under the other mappings (fewer steps)
+    # the same workload under the other mappings (fewer steps); forward: each
+    # mapping also with the other cluster setting
     by_mapping = {}
     for m in MAPS:
         if m == a.mapping:
             msm = ms_step
         else:
             msm, _, _ = timed(m, max(3, a.steps // 4), 2)
-        prof = load_profile_summary(a.workload, m) if a.pass_ == "fwd" else None
+        prof = load_profile_summary(a.workload, m, bool(a.cluster)) if a.pass_ == "fwd" else None
         by_mapping[m] = {"tflops": round(flops_job / (msm * 1e-3) / 1e12, 1), "ms_per_step": round(msm, 4),
                          "l2_hit_rate_pct": prof.get("lts__t_sector_hit_rate.pct") if prof else None}
+        if a.pass_ == "fwd":
+            cluster_on[0] = 1 - a.cluster
+            msc, _, _ = timed(m, max(3, a.steps // 4), 2)
+            cluster_on[0] = a.cluster
+            profc = load_profile_summary(a.workload, m, not a.cluster)
+            by_mapping[m]["cluster" if not a.cluster else "no_cluster"] = {
+                "tflops": round(flops_job / (msc * 1e-3) / 1e12, 1), "ms_per_step": round(msc, 4),
+                "l2_hit_rate_pct": profc.get("lts__t_sector_hit_rate.pct") if profc else None,
+                "dram_gb_per_launch": round(profc["dram_bytes_per_launch"] / 1e9, 3) if profc else None}
+            if prof:
+                by_mapping[m]["dram_gb_per_launch"] = round(prof["dram_bytes_per_launch"] / 1e9, 3)
 
     # end to end through the public API on pinned host buffers
     e2e_steps = max(2, min(a.steps, 10))
@@ -228,7 +243,8 @@ def run_ours(a):
         oh = torch.empty_like(qh).pin_memory()
 
         def e2e_step():
-            api.attn_fwd_host(qh, kh, vh, oh, causal=causal, scale=scale, mapping=a.mapping, stream=stream)
+            api.attn_fwd_host(qh, kh, vh, oh, causal=causal, scale=scale, mapping=a.mapping, stream=stream,
+                              cluster=bool(a.cluster))
         h2d = sum(t.numel() * t.element_size() for t in (qh, kh, vh))
         d2h = oh.numel() * oh.element_size()
         e2e_api = "attn_fwd_host (pinned host buffers, H2D + kernel + D2H + sync)"
@@ -262,7 +278,7 @@ def run_ours(a):
 
     peak, peak_sus, peak_src = load_peaks()
     achieved = flops_rank / (ms_kernel * 1e-3) / 1e12
-    prof = load_profile_summary(a.workload, a.mapping) if a.pass_ == "fwd" else None
+    prof = load_profile_summary(a.workload, a.mapping, bool(a.cluster)) if a.pass_ == "fwd" else None
     traffic = None
     if prof and prof.get("dram_bytes_per_launch") is not None:
         traffic = prof["dram_bytes_per_launch"]
@@ -273,6 +289,7 @@ def run_ours(a):
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (i.i.d. N(0,1) rounded to bf16, seeded per head)",
         "config": {"workload": a.workload, "B": B, "Hq": Hq_job, "Hkv": Hkv_job, "N": N, "d": d, "causal": causal,
                    "mapping": a.mapping, "pass": a.pass_, "heads_per_gpu": hq,
+                   "cluster_multicast": bool(a.cluster) and a.pass_ == "fwd",
                    "parallelism": f"heads sharded over {world} GPU(s), no data-path collective",
                    "l2": l2_note, "flop_convention": ("4*B*Hq*N^2*d, causal x0.5" if a.pass_ == "fwd" else
                                                       "10*B*Hq*N^2*d (5 matmuls), causal x0.5")},
@@ -412,6 +429,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--sets", type=int, default=0, help="resident input sets rotated per step (0: auto)")
     ap.add_argument("--flush", action="store_true", help="memset a 2xL2 buffer before every step")
+    ap.add_argument("--cluster", type=int, default=0, choices=(0, 1),
+                    help="forward as CTA-pair clusters with K/V multicast (ATTN_CLUSTER_MULTICAST, NEXT-4)")
     ap.add_argument("--pass", dest="pass_", default="fwd", choices=("fwd", "bwd"),
                     help="time the forward (default, the headline) or the backward (NEXT-3)")
     a = ap.parse_args()

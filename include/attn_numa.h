@@ -75,6 +75,17 @@ typedef enum {
  * only the schedule, never the result bits. */
 #define ATTN_ORDER_DESCENDING 0x100
 
+/* OR into `mapping` (forward only): run CTA pairs as thread-block clusters
+ * (NEXT-4, the ACC idea one level down: "CTAs that share K/V
+ * should run together").  The two CTAs of a cluster take adjacent work units
+ * that need the same K/V blocks -- the same unit of two query heads of one
+ * KV group when Hq/Hkv is even, else two adjacent units of one head -- and
+ * stream them once: each CTA TMA-loads half of every block and multicasts it
+ * to both, so a K/V block is read from L2 once per pair.  The mapping then
+ * orders the pairs ("cluster units").  Bit-identical results to the
+ * non-cluster path. */
+#define ATTN_CLUSTER_MULTICAST 0x200
+
 typedef enum {
   ATTN_OK = 0,
   ATTN_ERR_INVALID_VALUE = 1, /* null pointer, size <= 0, Hq % Hkv != 0, bad mapping value,
@@ -185,8 +196,11 @@ ATTN_API int attn_set_schedule_trace(int device, void* dev_buf, long long capaci
  * every queue q and position i, the unit (b, h, unit) into out[3*k..3*k+2]
  * in queue-major order and the queue lengths into queue_len[0..n_queues).
  * n_domains / sms_per_domain describe the dies (the active topology is not
- * consulted).  units_per_head = ceil(N / 256).  Returns INVALID_VALUE if
- * capacity (in units) is too small. */
+ * consulted).  units_per_head = ceil(N / 256).  With ATTN_CLUSTER_MULTICAST
+ * the entries are cluster units: if Hq/Hkv is even, (b, head pair p, unit u)
+ * = unit u of query heads 2p and 2p+1 (Hq/2 "heads"); otherwise (b, h, c) =
+ * units 2c and 2c+1 of head h (ceil(units_per_head / 2) per head).  Returns
+ * INVALID_VALUE if capacity (in units) is too small. */
 ATTN_API int attn_schedule_order(int B, int Hq, int Hkv, int N, int mapping, int n_domains, const int* sms_per_domain,
                         int32_t* out, long long capacity, int* n_queues, int* queue_len);
 

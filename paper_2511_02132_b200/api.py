@@ -34,14 +34,17 @@ def _check(rc: int) -> None:
 
 
 ORDER_DESCENDING = 0x100  # include/attn_numa.h ATTN_ORDER_DESCENDING
+CLUSTER_MULTICAST = 0x200  # include/attn_numa.h ATTN_CLUSTER_MULTICAST
 
 
-def _mapping_id(mapping, order: str = "ascending") -> int:
+def _mapping_id(mapping, order: str = "ascending", cluster: bool = False) -> int:
     m = mapping if isinstance(mapping, int) else MAPPINGS[str(mapping).lower()]
     if order == "descending":
         m |= ORDER_DESCENDING
     elif order != "ascending":
         raise ValueError("order must be 'ascending' or 'descending'")
+    if cluster:
+        m |= CLUSTER_MULTICAST
     return m
 
 
@@ -52,13 +55,15 @@ def _stream_ptr(stream: Optional[torch.cuda.Stream]) -> int:
 
 def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: Optional[torch.Tensor] = None, *,
              causal: bool = False, scale: Optional[float] = None, mapping="swizzled_head_first",
-             order: str = "ascending", stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+             order: str = "ascending", stream: Optional[torch.cuda.Stream] = None,
+             cluster: bool = False) -> torch.Tensor:
     """O = softmax(scale * Q K^T) V (PAPER.md eq:fa) on bf16 [B, H, N, d] CUDA tensors.
 
     q: [B, Hq, N, d]; k, v: [B, Hkv, N, d]; returns o [B, Hq, N, d] (allocated
     if not given).  scale defaults to 1/sqrt(d).  Asynchronous on `stream`
     (default: torch's current stream).  `order` = "descending" visits each
-    head's work units longest-first (ATTN_ORDER_DESCENDING); results are
+    head's work units longest-first (ATTN_ORDER_DESCENDING); `cluster` runs
+    CTA pairs that multicast K/V (ATTN_CLUSTER_MULTICAST).  Results are
     bit-identical either way.
     """
     for name, t in (("q", q), ("k", k), ("v", v)):
@@ -78,13 +83,14 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: Optional[torc
         scale = 1.0 / math.sqrt(d)
     lib = _lib.load()
     _check(lib.attn_fwd_stream(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), B, Hq, Hkv, N, d,
-                               int(bool(causal)), float(scale), _mapping_id(mapping, order), _stream_ptr(stream)))
+                               int(bool(causal)), float(scale), _mapping_id(mapping, order, cluster),
+                               _stream_ptr(stream)))
     return o
 
 
 def attn_fwd_lse(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool = False,
                  scale: Optional[float] = None, mapping="swizzled_head_first", order: str = "ascending",
-                 stream: Optional[torch.cuda.Stream] = None):
+                 stream: Optional[torch.cuda.Stream] = None, cluster: bool = False):
     """Forward that also returns the fp32 row log-sum-exp [B, Hq, N] (backward input)."""
     B, Hq, N, d = q.shape
     o = torch.empty_like(q)
@@ -93,7 +99,7 @@ def attn_fwd_lse(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: b
         scale = 1.0 / math.sqrt(d)
     lib = _lib.load()
     _check(lib.attn_fwd_lse(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), lse.data_ptr(), B, Hq,
-                            k.shape[1], N, d, int(bool(causal)), float(scale), _mapping_id(mapping, order),
+                            k.shape[1], N, d, int(bool(causal)), float(scale), _mapping_id(mapping, order, cluster),
                             _stream_ptr(stream)))
     return o, lse
 
@@ -127,7 +133,7 @@ def attn_bwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor,
 
 def attn_fwd_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor, *, causal: bool = False,
                   scale: Optional[float] = None, mapping="swizzled_head_first", order: str = "ascending",
-                  stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+                  stream: Optional[torch.cuda.Stream] = None, cluster: bool = False) -> torch.Tensor:
     """End-to-end call on HOST (ideally pinned) bf16 tensors: H2D, kernel, D2H, sync."""
     for t in (q, k, v, o):
         if t.is_cuda or t.dtype != torch.bfloat16 or not t.is_contiguous():
@@ -138,7 +144,8 @@ def attn_fwd_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Te
         scale = 1.0 / math.sqrt(d)
     lib = _lib.load()
     _check(lib.attn_fwd_host(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), B, Hq, Hkv, N, d,
-                             int(bool(causal)), float(scale), _mapping_id(mapping, order), _stream_ptr(stream)))
+                             int(bool(causal)), float(scale), _mapping_id(mapping, order, cluster),
+                             _stream_ptr(stream)))
     return o
 
 
@@ -195,7 +202,7 @@ def decode_trace(buf: torch.Tensor) -> torch.Tensor:
 
 
 def attn_schedule_order(B: int, Hq: int, Hkv: int, N: int, mapping, sms_per_domain: Sequence[int],
-                        order: str = "ascending") -> List[List[tuple]]:
+                        order: str = "ascending", cluster: bool = False) -> List[List[tuple]]:
     """Host-side queues (lists of (b, h, unit)) the kernel would pop (unit = 256 rows)."""
     lib = _lib.load()
     U = (N + 255) // 256
@@ -204,7 +211,7 @@ def attn_schedule_order(B: int, Hq: int, Hkv: int, N: int, mapping, sms_per_doma
     nq = ctypes.c_int(0)
     qlen = (ctypes.c_int * _lib.ATTN_MAX_DOMAINS)()
     sizes = (ctypes.c_int * len(sms_per_domain))(*sms_per_domain)
-    _check(lib.attn_schedule_order(B, Hq, Hkv, N, _mapping_id(mapping, order), len(sms_per_domain),
+    _check(lib.attn_schedule_order(B, Hq, Hkv, N, _mapping_id(mapping, order, cluster), len(sms_per_domain),
                                    ctypes.cast(sizes, ctypes.c_void_p), ctypes.cast(out, ctypes.c_void_p), cap,
                                    ctypes.cast(ctypes.pointer(nq), ctypes.c_void_p),
                                    ctypes.cast(qlen, ctypes.c_void_p)))

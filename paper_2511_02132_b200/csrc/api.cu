@@ -58,7 +58,8 @@ struct DevState {
   unsigned slot = 0;
   attn_trace_rec_t* trace = nullptr;
   long long trace_cap = 0;
-  bool attr_done[4] = {false, false, false, false};
+  bool attr_done[8] = {false, false, false, false, false, false, false, false};
+  int max_clusters[4] = {0, 0, 0, 0};  // co-resident CTA-pair clusters per forward variant
   // e2e host-buffer path
   void* hbuf[4] = {nullptr, nullptr, nullptr, nullptr};
   size_t hbuf_bytes[4] = {0, 0, 0, 0};
@@ -344,8 +345,9 @@ int validate(const void* q, const void* k, const void* v, void* o, int B, int Hq
   if (!q || !k || !v || !o) return fail(ATTN_ERR_INVALID_VALUE, "null pointer");
   if (B <= 0 || Hq <= 0 || Hkv <= 0 || N <= 0 || d <= 0) return fail(ATTN_ERR_INVALID_VALUE, "size <= 0");
   if (Hq % Hkv != 0) return fail(ATTN_ERR_INVALID_VALUE, "Hq % Hkv != 0 (non-uniform GQA groups)");
-  if ((mapping & ~(kMapMask | kOrderDescending)) || (mapping & kMapMask) > 3)
-    return fail(ATTN_ERR_INVALID_VALUE, "mapping not in {0,1,2,3} (| ATTN_ORDER_DESCENDING)");
+  if ((mapping & ~(kMapMask | kOrderDescending | ATTN_CLUSTER_MULTICAST)) || (mapping & kMapMask) > 3)
+    return fail(ATTN_ERR_INVALID_VALUE,
+                "mapping not in {0,1,2,3} (| ATTN_ORDER_DESCENDING | ATTN_CLUSTER_MULTICAST)");
   if (!std::isfinite(scale)) return fail(ATTN_ERR_INVALID_VALUE, "non-finite scale");
   const size_t qb = (size_t)B * Hq * N * d * 2, kb = (size_t)B * Hkv * N * d * 2;
   if (overlaps(o, qb, q, qb) || overlaps(o, qb, k, kb) || overlaps(o, qb, v, kb))
@@ -387,14 +389,42 @@ int make_tmap(CUtensorMap* m, const void* base, long long heads, int N, int d, i
 
 template <int D, bool kCausal>
 int launch_t(DevState& st, int attr_idx, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-             const KernelParams& kp, int grid, cudaStream_t s) {
-  auto* fn = attn_fwd_sm100_kernel<D, kCausal>;
+             const KernelParams& kp, int grid, cudaStream_t s, bool cluster, int cluster_units) {
   const int smem = Cfg<D>::kSmemBytes;
-  if (!st.attr_done[attr_idx]) {
-    ATTN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    st.attr_done[attr_idx] = true;
+  if (!cluster) {
+    auto* fn = attn_fwd_sm100_kernel<D, kCausal, 1>;
+    if (!st.attr_done[attr_idx]) {
+      ATTN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      st.attr_done[attr_idx] = true;
+    }
+    fn<<<grid, kThreads, smem, s>>>(tq, tk, tv, kp);
+  } else {
+    auto* fn = attn_fwd_sm100_kernel<D, kCausal, 2>;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (!st.attr_done[4 + attr_idx]) {
+      ATTN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      // persistent grid: as many pairs as can be co-resident (pairs need two
+      // free SMs of one GPC, so this can be below num_sms / 2)
+      cfg.gridDim = dim3(st.num_sms);
+      int nc = 0;
+      ATTN_CUDA(cudaOccupancyMaxActiveClusters(&nc, fn, &cfg));
+      st.max_clusters[attr_idx] = nc > 0 ? nc : st.num_sms / 2;
+      st.attr_done[4 + attr_idx] = true;
+    }
+    grid = 2 * std::min(st.max_clusters[attr_idx], cluster_units);
+    cfg.gridDim = dim3(grid);
+    ATTN_CUDA(cudaLaunchKernelEx(&cfg, fn, tq, tk, tv, kp));
   }
-  fn<<<grid, kThreads, smem, s>>>(tq, tk, tv, kp);
   ATTN_CUDA(cudaGetLastError());
   g_info.grid = grid;
   g_info.block = kThreads;
@@ -423,14 +453,25 @@ int fwd_impl(const void* q, const void* k, const void* v, void* o, int B, int Hq
 
   const int nblk = (N + kBlockM - 1) / kBlockM;  // last block may be ragged
   const int U = (nblk + 1) / 2;
+  const bool cluster = (mapping & ATTN_CLUSTER_MULTICAST) != 0;
+  mapping &= ~ATTN_CLUSTER_MULTICAST;
+  // cluster units: with an even GQA group the pair takes the same unit of two
+  // query heads of one KV group (identical K/V blocks); otherwise two adjacent
+  // units of one head
+  const bool pair_heads = cluster && (Hq / Hkv) % 2 == 0;
+  const int Usched = (cluster && !pair_heads) ? (U + 1) / 2 : U;
+  const int Hsched = pair_heads ? Hq / 2 : Hq;
   KernelParams kp{};
   kp.B = B; kp.Hq = Hq; kp.Hkv = Hkv; kp.N = N; kp.G = Hq / Hkv; kp.U = U; kp.nblk = nblk;
+  kp.Usched = Usched;
+  kp.Hsched = Hsched;
+  kp.pair_heads = pair_heads ? 1 : 0;
   kp.d_real = d;
   const int dpad = d <= 64 ? 64 : 128;  // kernel head dim; TMA zero-fills columns d..dpad-1
   kp.scale_log2 = scale * 1.4426950408889634f;
   kp.o = reinterpret_cast<__nv_bfloat16*>(o);
   kp.lse = lse;
-  if (!build_sched(mapping, B, Hq, Hkv, U, st.active.n_domains, st.active.sms_per_domain, kp.sched))
+  if (!build_sched(mapping, B, Hsched, Hkv, Usched, st.active.n_domains, st.active.sms_per_domain, kp.sched))
     return fail(ATTN_ERR_INVALID_VALUE, "cannot build the schedule");
   const unsigned slot = st.slot++ % kCounterSlots;
   kp.counters = st.d_counters + (size_t)slot * kCounterInts;
@@ -441,15 +482,18 @@ int fwd_impl(const void* q, const void* k, const void* v, void* o, int B, int Hq
 
   CUtensorMap tq, tk, tv;
   if ((rc = make_tmap(&tq, q, (long long)B * Hq, N, d, kBlockM)) != ATTN_OK) return rc;
-  if ((rc = make_tmap(&tk, k, (long long)B * Hkv, N, d, kBlockN)) != ATTN_OK) return rc;
-  if ((rc = make_tmap(&tv, v, (long long)B * Hkv, N, d, kBlockN)) != ATTN_OK) return rc;
+  // clusters: each CTA of a pair loads half the rows of every K/V block
+  const int kv_box = cluster ? kBlockN / 2 : kBlockN;
+  if ((rc = make_tmap(&tk, k, (long long)B * Hkv, N, d, kv_box)) != ATTN_OK) return rc;
+  if ((rc = make_tmap(&tv, v, (long long)B * Hkv, N, d, kv_box)) != ATTN_OK) return rc;
 
   const int total = B * Hq * U;
+  const int cunits = B * Hsched * Usched;
   const int grid = std::min(st.num_sms, total);
-  if (dpad == 128 && causal) rc = launch_t<128, true>(st, 0, tq, tk, tv, kp, grid, stream);
-  else if (dpad == 128) rc = launch_t<128, false>(st, 1, tq, tk, tv, kp, grid, stream);
-  else if (causal) rc = launch_t<64, true>(st, 2, tq, tk, tv, kp, grid, stream);
-  else rc = launch_t<64, false>(st, 3, tq, tk, tv, kp, grid, stream);
+  if (dpad == 128 && causal) rc = launch_t<128, true>(st, 0, tq, tk, tv, kp, grid, stream, cluster, cunits);
+  else if (dpad == 128) rc = launch_t<128, false>(st, 1, tq, tk, tv, kp, grid, stream, cluster, cunits);
+  else if (causal) rc = launch_t<64, true>(st, 2, tq, tk, tv, kp, grid, stream, cluster, cunits);
+  else rc = launch_t<64, false>(st, 3, tq, tk, tv, kp, grid, stream, cluster, cunits);
   if (rc != ATTN_OK) return rc;
   g_info.units = total;
   g_info.n_queues = kp.sched.n_queues;
@@ -483,6 +527,7 @@ int bwd_impl(const void* q, const void* k, const void* v, const void* o, const v
              cudaStream_t stream) {
   int rc = validate(q, k, v, dq, B, Hq, Hkv, N, d, scale, mapping);
   if (rc != ATTN_OK) return rc;
+  if (mapping & ATTN_CLUSTER_MULTICAST) return fail(ATTN_ERR_UNSUPPORTED, "ATTN_CLUSTER_MULTICAST is forward-only");
   if (!o || !dout || !lse || !dk || !dv) return fail(ATTN_ERR_INVALID_VALUE, "null pointer");
   const size_t qb = (size_t)B * Hq * N * d * 2, kb = (size_t)B * Hkv * N * d * 2, lb = (size_t)B * Hq * N * 4;
   for (const void* out : {(const void*)dq, (const void*)dk, (const void*)dv}) {
@@ -740,7 +785,12 @@ int attn_schedule_order(int B, int Hq, int Hkv, int N, int mapping, int n_domain
                         int32_t* out, long long capacity, int* n_queues, int* queue_len) {
   if (!out || !n_queues || !queue_len || !sms_per_domain) return fail(ATTN_ERR_INVALID_VALUE, "null pointer");
   if (B <= 0 || Hq <= 0 || Hkv <= 0 || N <= 0 || Hq % Hkv) return fail(ATTN_ERR_INVALID_VALUE, "bad sizes");
-  const int U = (N + 255) / 256;
+  // ATTN_CLUSTER_MULTICAST: the queues hold cluster units -- (b, head pair,
+  // unit) when Hq/Hkv is even, else (b, head, pair of adjacent units)
+  const bool cl = (mapping & ATTN_CLUSTER_MULTICAST) != 0, pair_heads = cl && (Hq / Hkv) % 2 == 0;
+  const int U = (cl && !pair_heads) ? ((N + 255) / 256 + 1) / 2 : (N + 255) / 256;
+  if (pair_heads) Hq /= 2;
+  mapping &= ~ATTN_CLUSTER_MULTICAST;
   SchedParams sp;
   if (!build_sched(mapping, B, Hq, Hkv, U, n_domains, sms_per_domain, sp))
     return fail(ATTN_ERR_INVALID_VALUE, "bad mapping or domains");

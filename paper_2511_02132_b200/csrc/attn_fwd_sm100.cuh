@@ -98,6 +98,10 @@ struct Cfg {
 
 struct KernelParams {
   int B, Hq, Hkv, N, G, U, nblk;
+  int Usched;        // units per head in the queues: U, or ceil(U/2) cluster units (kCl == 2, adjacent mode)
+  int Hsched;        // heads in the queues: Hq, or Hq/2 head pairs (kCl == 2, head-pair mode)
+  int pair_heads;    // kCl == 2: 1 = the pair takes unit u of query heads 2h', 2h'+1 (one KV group);
+                     //           0 = the pair takes units 2u', 2u'+1 of one head
   int d_real;        // head dim of the tensors (<= D; TMA zero-fills columns d_real..D-1)
   float scale_log2;  // scale * log2(e), >= 0
   __nv_bfloat16* o;
@@ -141,20 +145,71 @@ __device__ __forceinline__ void unit_blocks(int u, int nblk, int& n0, int& n1) {
   }
 }
 
+// Consumer side of the scheduler ring.  kCl == 2 (CTA-pair clusters): the
+// entries are written by the leader CTA's scheduler into both CTAs, and every
+// consumer of both CTAs releases the slot on the LEADER's sched_empty.
+template <int kCl>
 struct SchedReader {
   int stage = 0;
   uint32_t phase = 0;
+  __device__ __forceinline__ void release(Ctrl* c, int st) {
+    if constexpr (kCl == 1) ptx::mbar_arrive(&c->sched_empty[st]);
+    else ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&c->sched_empty[st]), 0));
+  }
   __device__ __forceinline__ int4 next(Ctrl* c, bool arrive) {
-    ptx::mbar_wait(&c->sched_full[stage], phase);
+    if constexpr (kCl == 1) ptx::mbar_wait(&c->sched_full[stage], phase);
+    else ptx::mbar_wait_cluster(&c->sched_full[stage], phase);
     const volatile int* ve = reinterpret_cast<const volatile int*>(&c->entry[stage]);
     const int4 e = make_int4(ve[0], ve[1], ve[2], ve[3]);
-    if (arrive) ptx::mbar_arrive(&c->sched_empty[stage]);
+    if (arrive) release(c, stage);
     if (++stage == kSchedRing) { stage = 0; phase ^= 1; }
     return e;
   }
+  __device__ __forceinline__ void release_prev(Ctrl* c) { release(c, (stage + kSchedRing - 1) % kSchedRing); }
 };
 
-template <int D, bool kCausal>
+// This CTA's (head, unit) of a scheduler entry (b, h, u, w).  kCl == 1: (h, u).
+// kCl == 2, head pairs: (2h + rank, u) -- both query heads of one KV group, so
+// the pair needs exactly the same K/V blocks; adjacent units: (h, 2u + rank),
+// unit -1 when the pair has only one unit.
+template <int kCl>
+__device__ __forceinline__ int own_unit(const int4& e, uint32_t crank, int U, int pair_heads, int& head) {
+  if constexpr (kCl == 1) {
+    head = e.y;
+    return e.z;
+  }
+  if (pair_heads) {
+    head = 2 * e.y + (int)crank;
+    return e.z;
+  }
+  head = e.y;
+  const int u = 2 * e.z + (int)crank;
+  return u < U ? u : -1;
+}
+// K/V blocks the cluster streams for entry e: the longer unit of the pair.
+template <bool kCausal>
+__device__ __forceinline__ int pair_kv_blocks(const int4& e, const KernelParams& p);
+template <bool kCausal>
+__device__ __forceinline__ int unit_kv_blocks(int u, int nblk) {
+  if (u < 0) return 0;
+  int n0, n1;
+  unit_blocks<kCausal>(u, nblk, n0, n1);
+  return n0 > n1 ? n0 : n1;
+}
+template <bool kCausal>
+__device__ __forceinline__ int pair_kv_blocks(const int4& e, const KernelParams& p) {
+  if (p.pair_heads) return unit_kv_blocks<kCausal>(e.z, p.nblk);
+  return max(unit_kv_blocks<kCausal>(2 * e.z, p.nblk),
+             unit_kv_blocks<kCausal>(2 * e.z + 1 < p.U ? 2 * e.z + 1 : -1, p.nblk));
+}
+
+// kCl == 2: CTA-pair clusters (NEXT-4).  The pair works on the two halves of
+// one cluster unit (units 2cu, 2cu+1 of the same head) and streams the SAME K/V
+// blocks: each CTA TMA-loads half the rows of every block and multicasts them
+// to both, and each MMA warp releases a ring slot to both CTAs' kv_empty.  The
+// pair iterates over the longer unit's key blocks; the CTA whose own unit is
+// shorter (causal) only releases the extra slots.
+template <int D, bool kCausal, int kCl>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                           const __grid_constant__ CUtensorMap tm_v, const KernelParams p) {
@@ -169,19 +224,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   static_assert(kSplit == 1 || C::kCtrlBytes >= 1024 + (int)sizeof(SplitRed), "split reductions do not fit");
   static_assert(C::kSmemBytes <= 232448, "shared memory exceeds 227 KB");
 
+  static_assert(kCl == 1 || kCl == 2, "cluster size 1 or 2");
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t crank = (kCl > 1) ? ptx::cluster_ctarank() : 0u;
+  constexpr uint16_t kMask = (1u << kCl) - 1;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kSchedRing; ++i) {
       ptx::mbar_init(&ctrl->sched_full[i], 1);
-      ptx::mbar_init(&ctrl->sched_empty[i], 2 + kSoftmaxWarps);  // TMA + MMA + softmax warps (one arrive each)
+      // TMA + MMA + softmax warps (one arrive each), of every CTA of the cluster
+      ptx::mbar_init(&ctrl->sched_empty[i], kCl * (2 + kSoftmaxWarps));
     }
     ptx::mbar_init(&ctrl->q_full, 1);
     ptx::mbar_init(&ctrl->q_empty, 1);
     for (int i = 0; i < C::kStages; ++i) {
       ptx::mbar_init(&ctrl->kv_full[i], 1);
-      ptx::mbar_init(&ctrl->kv_empty[i], 1);
+      ptx::mbar_init(&ctrl->kv_empty[i], kCl);  // released by the MMA warp of every CTA of the cluster
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&ctrl->s_ready[i], 1);
@@ -202,13 +261,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   ptx::tc_fence_before();
   __syncthreads();
+  if constexpr (kCl > 1) ptx::cluster_sync();  // peer barriers initialised before any remote arrive / multicast
   ptx::tc_fence_after();
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (ATTN_SETMAXNREG) ptx::setmaxnreg_dec<kOtherRegs>();
     if (lane == 0) {
-      SchedReader sr;
+      SchedReader<kCl> sr;
       const uint64_t pol_q = ptx::policy_evict_first();
 #if ATTN_KV_EVICT_LAST
       const uint64_t pol_kv = ptx::policy_evict_last();
@@ -218,13 +278,33 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t q_phase = 0;
       int kv_stage = 0;
       uint32_t kv_phase = 0;
+      [[maybe_unused]] int seq = 0;
       while (true) {
         const int4 e = sr.next(ctrl, true);
         if (!e.w) break;
-        const int b = e.x, h = e.y, u = e.z;
-        int n0, n1;
-        unit_blocks<kCausal>(u, p.nblk, n0, n1);
-        const int n = n0 > n1 ? n0 : n1;
+        int h;
+        const int b = e.x, u = own_unit<kCl>(e, crank, p.U, p.pair_heads, h);
+        int n0 = 0, n1 = 0;
+        if (u >= 0) unit_blocks<kCausal>(u, p.nblk, n0, n1);
+        const int n_own = n0 > n1 ? n0 : n1;
+        // key blocks the cluster streams: the longer of the pair's units
+        const int n = (kCl == 1) ? n_own : pair_kv_blocks<kCausal>(e, p);
+        if constexpr (kCl > 1) {
+          if (p.trace && u >= 0) {
+            const long long id = ((long long)b * p.Hq + h) * p.U + u;
+            if (id < p.trace_cap) {
+              const int sm = (int)ptx::smid();
+              attn_trace_rec_t r;
+              r.b = b; r.h = h; r.unit = u; r.smid = sm;
+              r.domain = (sm < p.n_smid) ? (int)p.domain_of_smid[sm] : 0;
+              r.queue = (e.w >> 1) & 63; r.stolen = (e.w >> 7) & 1; r.seq = seq;
+              r.t_pop_ns = ptx::globaltimer();
+              p.trace[id] = r;
+            }
+          }
+          ++seq;
+        }
+        if (n_own > 0) {
         ptx::mbar_wait(&ctrl->q_empty, q_phase ^ 1);
         q_phase ^= 1;
         const int ntile = n1 > 0 ? 2 : 1;
@@ -242,11 +322,24 @@ __global__ void __launch_bounds__(kThreads, 1)
                              pol_q);
 #endif
         }
+        }
         const int kvbh = b * p.Hkv + h / p.G;
         for (int j = 0; j < n; ++j) {
 #pragma unroll
           for (int which = 0; which < 2; ++which) {
             ptx::mbar_wait(&ctrl->kv_empty[kv_stage], kv_phase ^ 1);
+            if constexpr (kCl > 1) {
+              // this CTA's half of the block's rows, multicast into both CTAs
+              ptx::mbar_arrive_expect_tx(&ctrl->kv_full[kv_stage], C::kKVBytes);
+              uint8_t* dst = kv_smem + kv_stage * C::kKVBytes + crank * (kBlockN / 2) * 128;
+#pragma unroll
+              for (int c = 0; c < C::kChunks; ++c)
+                ptx::tma_load_3d_mc(dst + c * kBlockN * 128, which == 0 ? (const void*)&tm_k : (const void*)&tm_v,
+                                    &ctrl->kv_full[kv_stage], c * 64, j * kBlockN + (int)crank * (kBlockN / 2), kvbh,
+                                    kMask, pol_kv);
+              if (++kv_stage == C::kStages) { kv_stage = 0; kv_phase ^= 1; }
+              continue;
+            }
 #ifdef ATTN_DEBUG_NO_KV_LOAD
             if (j >= 2) {  // bandwidth probe: reuse whatever is in the slot
               ptx::mbar_arrive(&ctrl->kv_full[kv_stage]);
@@ -269,6 +362,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      if constexpr (kCl > 1) {
+        // drain: every slot's last fill released by both CTAs, so no remote
+        // commit is still in flight towards this CTA when it exits
+        for (int i = 0; i < C::kStages; ++i) {
+          ptx::mbar_wait(&ctrl->kv_empty[kv_stage], kv_phase ^ 1);
+          if (++kv_stage == C::kStages) { kv_stage = 0; kv_phase ^= 1; }
+        }
+      }
     }
   } else if (warp == 1) {
     // -------------------------------------------------------------- MMA issuer
@@ -276,7 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // uniform registers); one elected lane issues tcgen05.mma / commit.
     if (ATTN_SETMAXNREG) ptx::setmaxnreg_dec<kOtherRegs>();
     const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(&ctrl->tmem_base);
-    SchedReader sr;
+    SchedReader<kCl> sr;
     constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(kBlockM, kBlockN, 0, 0);
 #ifdef ATTN_DEBUG_PV_KMAJOR
     constexpr uint32_t idesc_o = ptx::idesc_bf16_f32(kBlockM, D, 0, 0);  // wrong layout: speed probe only
@@ -291,6 +392,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t dv0 = ptx::smem_desc_sw128(ptx::smem_u32(kv_smem), kBlockN * 128, 1024);
     uint32_t q_phase = 0, p_phase0 = 0, p_phase1 = 0;
     [[maybe_unused]] int unit_no = -1;
+    [[maybe_unused]] int extra_blocks = 0;
     int kv_stage = 0;
     uint32_t kv_phase = 0;
 
@@ -333,16 +435,37 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (++kv_stage == C::kStages) { kv_stage = 0; kv_phase ^= 1; }
       return s;
     };
+    // release a K/V ring slot (to every CTA of the cluster) once the MMAs
+    // issued so far have completed
+    auto kv_release = [&](int s) {
+      if constexpr (kCl == 1) ptx::mma_commit(&ctrl->kv_empty[s]);
+      else ptx::mma_commit_mc(&ctrl->kv_empty[s], kMask);
+    };
 
     while (true) {
       int4 e;
       ATTN_TIMED(w_sched, e = sr.next(ctrl, false));
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&ctrl->sched_empty[(sr.stage + kSchedRing - 1) % kSchedRing]);
+      if (lane == 0) sr.release_prev(ctrl);
       if (!e.w) break;
-      int n0, n1;
-      unit_blocks<kCausal>(e.z, p.nblk, n0, n1);
+      int hu;
+      const int u = own_unit<kCl>(e, crank, p.U, p.pair_heads, hu);
+      int n0 = 0, n1 = 0;
+      if (u >= 0) unit_blocks<kCausal>(u, p.nblk, n0, n1);
       const int n = n0 > n1 ? n0 : n1;
+      if constexpr (kCl > 1) {
+        // blocks the pair streams beyond this CTA's own unit: take and release
+        const int n_all = pair_kv_blocks<kCausal>(e, p);
+        if (n == 0) {
+          for (int j = 0; j < n_all; ++j) {
+            const int a = take_slot(), b2 = take_slot();
+            if (ptx::elect_one_sync()) { kv_release(a); kv_release(b2); }
+            __syncwarp();
+          }
+          continue;
+        }
+        extra_blocks = n_all - n;
+      }
       ATTN_TIMED(w_q, ptx::mbar_wait(&ctrl->q_full, q_phase));
       ++unit_no;
       q_phase ^= 1;
@@ -357,7 +480,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           issue_s(1, sK);
           ptx::mma_commit(&ctrl->s_ready[1]);
         }
-        ptx::mma_commit(&ctrl->kv_empty[sK]);
+        kv_release(sK);
         if (n == 1) ptx::mma_commit(&ctrl->q_empty);
       }
       __syncwarp();
@@ -403,13 +526,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         if (ptx::elect_one_sync()) {
-          ptx::mma_commit(&ctrl->kv_empty[sV]);
+          kv_release(sV);
           if (nxt) {
-            ptx::mma_commit(&ctrl->kv_empty[sK]);
+            kv_release(sK);
             if (j + 2 == n) ptx::mma_commit(&ctrl->q_empty);
           }
         }
         __syncwarp();
+      }
+      if constexpr (kCl > 1) {
+        for (int j = 0; j < extra_blocks; ++j) {
+          const int a = take_slot(), b2 = take_slot();
+          if (ptx::elect_one_sync()) { kv_release(a); kv_release(b2); }
+          __syncwarp();
+        }
+        extra_blocks = 0;
       }
     }
 #ifdef ATTN_PROFILE_WAITS
@@ -421,7 +552,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 2) {
     // --------------------------------------------------------------- scheduler
     if (ATTN_SETMAXNREG) ptx::setmaxnreg_dec<kOtherRegs>();
-    if (lane == 0) {
+    if (lane == 0 && crank == 0) {  // clusters: the leader CTA schedules for the pair
       const int sm = (int)ptx::smid();
       int dom = (sm < p.n_smid) ? (int)p.domain_of_smid[sm] : 0;
       if (dom < 0) dom = 0;
@@ -439,20 +570,31 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (exhausted & (1u << qq)) continue;
           const int pos = atomicAdd(&p.counters[qq * 32], 1);
           if (pos < p.sched.q[qq].len) {
-            decode_unit(p.sched.q[qq], pos, p.Hq, p.U, b, h, u);
-            if (p.sched.descending) u = p.U - 1 - u;
+            decode_unit(p.sched.q[qq], pos, p.Hsched, p.Usched, b, h, u);
+            if (p.sched.descending) u = p.Usched - 1 - u;
             qi = qq;
             stolen = t > 0;
             break;
           }
           exhausted |= 1u << qq;
         }
-        ptx::mbar_wait(&ctrl->sched_empty[stage], phase ^ 1);
-        ctrl->entry[stage] = make_int4(b, h, u, qi >= 0 ? 1 : 0);
-        ptx::mbar_arrive(&ctrl->sched_full[stage]);
+        if constexpr (kCl == 1) {
+          ptx::mbar_wait(&ctrl->sched_empty[stage], phase ^ 1);
+          ctrl->entry[stage] = make_int4(b, h, u, qi >= 0 ? 1 : 0);
+          ptx::mbar_arrive(&ctrl->sched_full[stage]);
+        } else {
+          // both CTAs' consumers released the slot on this (leader) CTA's barrier;
+          // w packs valid | queue << 1 | stolen << 7 for the peers' trace records
+          ptx::mbar_wait_cluster(&ctrl->sched_empty[stage], phase ^ 1);
+          const int4 ent = make_int4(b, h, u, qi >= 0 ? (1 | (qi << 1) | (stolen << 7)) : 0);
+          ctrl->entry[stage] = ent;
+          ptx::st_cluster_v4(ptx::mapa_shared(ptx::smem_u32(&ctrl->entry[stage]), 1), ent);
+          ptx::mbar_arrive(&ctrl->sched_full[stage]);
+          ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&ctrl->sched_full[stage]), 1));
+        }
         if (qi < 0) break;
 #ifndef ATTN_PROFILE_WAITS
-        if (p.trace) {
+        if (kCl == 1 && p.trace) {
           const long long id = ((long long)b * p.Hq + h) * p.U + u;
           if (id < p.trace_cap) {
             attn_trace_rec_t r;
@@ -468,7 +610,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // Self-resetting counters: the last CTA to finish popping zeroes the
       // queue counters for the next launch on this slot (no host memset).
       __threadfence();
-      if (atomicAdd(&p.counters[kDoneCounter], 1) == (int)gridDim.x - 1) {
+      if (atomicAdd(&p.counters[kDoneCounter], 1) == (int)gridDim.x / kCl - 1) {
         for (int q = 0; q < nq; ++q) atomicExch(&p.counters[q * 32], 0);
         atomicExch(&p.counters[kDoneCounter], 0);
         __threadfence();
@@ -495,18 +637,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 #if ATTN_O_EVICT_FIRST
     const uint64_t pol_o = ptx::policy_evict_first();
 #endif
-    SchedReader sr;
+    SchedReader<kCl> sr;
     uint32_t s_phase = 0, o_phase = 0, gblk = 0;
     while (true) {
       const int4 e = sr.next(ctrl, false);
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&ctrl->sched_empty[(sr.stage + kSchedRing - 1) % kSchedRing]);
+      if (lane == 0) sr.release_prev(ctrl);
       if (!e.w) break;
-      int n0, n1;
-      unit_blocks<kCausal>(e.z, p.nblk, n0, n1);
+      int hh;
+      const int u = own_unit<kCl>(e, crank, p.U, p.pair_heads, hh);
+      int n0 = 0, n1 = 0;
+      if (u >= 0) unit_blocks<kCausal>(u, p.nblk, n0, n1);
       const int nt = (t == 0) ? n0 : n1;
       if (nt == 0) continue;
-      const int qb = 2 * e.z + t;
+      const int qb = 2 * u + t;
       // keys of the last key block that exist (ragged N): local key k < tail_keys
       const int last_blk = p.nblk - 1;
       const int tail_lim = (p.N - last_blk * kBlockN - 1) - cbase;  // last block: local k visible iff k <= tail_lim
@@ -644,8 +788,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::tc_fence_after();
       const float inv_l = 1.f / l;
       if (p.lse != nullptr && hf == 0 && qb * kBlockM + row < p.N)  // lse = scale*m + ln(l)
-        p.lse[(long long)(e.x * p.Hq + e.y) * p.N + qb * kBlockM + row] = (m * c + __log2f(l)) * 0.6931471805599453f;
-      const long long orow = ((long long)(e.x * p.Hq + e.y) * p.N + (long long)qb * kBlockM + row) * p.d_real;
+        p.lse[(long long)(e.x * p.Hq + hh) * p.N + qb * kBlockM + row] = (m * c + __log2f(l)) * 0.6931471805599453f;
+      const long long orow = ((long long)(e.x * p.Hq + hh) * p.N + (long long)qb * kBlockM + row) * p.d_real;
       uint4* dst = reinterpret_cast<uint4*>(p.o + orow + hf * kOCols);
       // real columns of this thread's slice (multiple of 8); rows >= N (ragged
       // last query block) store nothing but still join the warp-wide TMEM loads
@@ -676,6 +820,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   ptx::tc_fence_before();
   __syncthreads();
+  if constexpr (kCl > 1) ptx::cluster_sync();  // no remote SMEM access may target an exited CTA
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(*reinterpret_cast<volatile uint32_t*>(&ctrl->tmem_base), kTmemCols);

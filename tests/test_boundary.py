@@ -48,7 +48,7 @@ def _fwd(lib, q=1 << 20, k=2 << 20, v=3 << 20, o=4 << 20, B=1, Hq=2, Hkv=2, N=12
 
 @pytest.mark.parametrize("kw,status", [
     (dict(q=0), 1), (dict(o=0), 1), (dict(B=0), 1), (dict(N=-1), 1), (dict(Hq=6, Hkv=4), 1),
-    (dict(mapping=4), 1), (dict(mapping=-1), 1), (dict(mapping=0x200), 1), (dict(mapping=0x104), 1), (dict(scale=float("nan")), 1), (dict(scale=float("inf")), 1),
+    (dict(mapping=4), 1), (dict(mapping=-1), 1), (dict(mapping=0x400), 1), (dict(mapping=0x204), 1), (dict(mapping=0x104), 1), (dict(scale=float("nan")), 1), (dict(scale=float("inf")), 1),
     (dict(d=100), 2), (dict(d=136), 2), (dict(scale=-0.5), 2), (dict(q=(1 << 20) + 8), 2),
     (dict(o=(1 << 20) + 64), 1),   # o overlaps q
 ])
@@ -95,6 +95,30 @@ def test_schedule_order_descending_matches_oracle(lib):
         for m in om.MAPPINGS:
             got = api.attn_schedule_order(B, Hq, Hkv, N, m, [74, 74], order="descending")
             assert got == om.descending(om.build_queues(m, B, Hq, Hkv, U, [74, 74]), U)
+
+
+def test_schedule_order_cluster_units_match_oracle(lib):
+    """ATTN_CLUSTER_MULTICAST: the queues order cluster units exactly as the
+    mapping oracle orders units -- head pairs of one KV group (Hq/2 "heads")
+    when Hq/Hkv is even, else pairs of adjacent units (ceil(U/2) per head)."""
+    rng = random.Random(13)
+    for _ in range(40):
+        Hkv = rng.choice([1, 2, 3, 4, 8])
+        Hq = Hkv * rng.choice([1, 2, 3, 4])
+        B, N = rng.randint(1, 2), 128 * rng.randint(1, 12)
+        U = (N + 255) // 256
+        for m in om.MAPPINGS:
+            got = api.attn_schedule_order(B, Hq, Hkv, N, m, [74, 74], cluster=True)
+            if (Hq // Hkv) % 2 == 0:
+                assert got == om.build_queues(m, B, Hq // 2, Hkv, U, [74, 74])
+            else:
+                assert got == om.build_queues(m, B, Hq, Hkv, (U + 1) // 2, [74, 74])
+
+
+def test_backward_rejects_cluster_flag(lib):
+    fake = [(i + 1) << 20 for i in range(9)]
+    rc = lib.attn_bwd(*fake, 1, 2, 2, 128, 64, 0, 0.125, 2 | 0x200, None)
+    assert rc == 2 and b"forward-only" in lib.attn_last_error()
 
 
 def test_schedule_order_baseline_configs(lib):
