@@ -665,7 +665,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef ATTN_TIMELINE
         long long* tls = (p.trace && blockIdx.x == 0 && quarter == 0 && lane == 0 && first_unit && j < 64)
                              ? reinterpret_cast<long long*>(p.trace) + 600 + t * 200 + j * 3 : nullptr;
+        // fine stamps: [s_wake, ld done, max done, P half 0, P half 1, sum done]
+        long long* tl2 = (p.trace && blockIdx.x == 0 && quarter == 0 && lane == 0 && first_unit && j < 64)
+                             ? reinterpret_cast<long long*>(p.trace) + 4096 + t * 512 + j * 8 : nullptr;
         if (tls) tls[0] = clock64();
+        if (tl2) tl2[0] = clock64();
 #endif
 #ifdef ATTN_DEBUG_SKIP_SOFTMAX
         __syncwarp();
@@ -676,6 +680,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t r[kCols];
         if constexpr (kCols == 128) ptx::tmem_ld128(trow + colS, r);
         else ptx::tmem_ld64(trow + colS, r);
+#ifdef ATTN_TIMELINE
+        if (tl2) tl2[1] = clock64() + (r[0] & 0) + (r[kCols - 1] & 0);
+#endif
         // visible local keys are k <= lim: causal diagonal block (key <= query)
         // and/or the ragged last key block (key < N)
         int lim = kCols;
@@ -697,6 +704,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             mq[g4] = fmaxf(mq[g4], fmaxf(__uint_as_float(r[k + 2 * g4]), __uint_as_float(r[k + 2 * g4 + 1])));
         }
         float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
+#ifdef ATTN_TIMELINE
+        if (tl2) tl2[2] = clock64() + (long long)(mx == 12345.f);
+#endif
         if constexpr (kSplit == 2) {
           sred->red[t][quarter][hf][gblk & 1][lane] = mx;
           ptx::named_bar_sync(bar_id, 64);
@@ -766,6 +776,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) ptx::mbar_arrive(&ctrl->p_ready[t][h]);
 #ifdef ATTN_TIMELINE
           if (tls) tls[1 + h] = clock64();
+          if (tl2) tl2[3 + h] = clock64();
 #endif
         }
         };
@@ -773,6 +784,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         else exp_block(std::false_type{});
         const float2 s01 = ptx::fadd2(sq[0], sq[1]), s23 = ptx::fadd2(sq[2], sq[3]);
         const float2 s4 = ptx::fadd2(s01, s23);
+#ifdef ATTN_TIMELINE
+        if (tl2) tl2[5] = clock64() + (long long)(s4.x == 12345.f);
+#endif
         const float sum = s4.x + s4.y;
         l = (j == 0) ? sum : fmaf(l, alpha, sum);
         m = m_use;

@@ -9,7 +9,7 @@ from paper_2511_02132_b200 import attn_fwd, attn_set_schedule_trace, synth
 
 q, k, v = synth.make_qkv(1, 32, 32, 8192, 128, base=0, device="cuda")
 attn_fwd(q, k, v)
-buf = torch.zeros(2048 * 2, dtype=torch.int32, device="cuda")
+buf = torch.zeros(8192 * 2, dtype=torch.int32, device="cuda")
 attn_set_schedule_trace(0, buf)
 attn_fwd(q, k, v, mapping="swizzled_head_first")
 torch.cuda.synchronize()
@@ -29,3 +29,9 @@ print("softmax0 s_wake -> p_h1 (median):", int(np.median(sm0[8:60, 2] - sm0[8:60
       " softmax1:", int(np.median(sm1[8:60, 2] - sm1[8:60, 0])))
 print("t0 issue done -> softmax0 next s_wake (median):", int(np.median(sm0[9:61, 0] - mma[8:60, 3])))
 print("softmax0 p_h1 -> MMA p0_ok (median):", int(np.median(mma[9:61, 2] - sm0[9:61, 2])))
+# fine softmax stamps (tile 0 and 1): s_wake, ld done, max done, P half 0, P half 1, sum done
+for tt in (0, 1):
+    f = t[4096 + tt * 512: 4096 + tt * 512 + 64 * 8].reshape(64, 8)[:, :6] - t0
+    dd = np.median(np.diff(f[8:60], axis=1), axis=0).astype(int)
+    print(f"tile {tt} softmax phases (median cycles): ld {dd[0]}  max {dd[1]}  exp+st half0 {dd[2]}  "
+          f"exp+st half1 {dd[3]}  sum {dd[4]}  total {int(np.median(f[8:60, 5] - f[8:60, 0]))}")
