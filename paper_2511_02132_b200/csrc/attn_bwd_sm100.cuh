@@ -646,18 +646,24 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
       const int b = e.x, g = e.y, j = e.z;
       const int kglob = j * kBM + krow;
       const int i0 = dkdv_first_qblock<kCausal>(j);
+      // lse (as log2) and D of each block's 128 queries are staged in SMEM
+      // (double-buffered by block parity); thread et stages one value, which
+      // it loads from global one block ahead so the L2 latency stays hidden
+      const int qq = et & (kBM - 1);
+      auto stage_load = [&](int hh_, int i_) -> float {
+        const long long vi = (long long)(b * p.Hq + g * p.G + hh_) * p.N + i_ * kBM;
+        if (i_ * kBM + qq >= p.N) return 0.f;
+        return et < kBM ? __ldg(p.lse + vi + qq) * 1.4426950408889634f : __ldg(p.dvec + vi + qq);
+      };
+      float staged = stage_load(0, i0);
       for (int hh = 0; hh < p.G; ++hh) {
         for (int i = i0; i < p.nblk; ++i) {
-          // lse (as log2) and D of this block's 128 queries, staged in SMEM
-          // (double-buffered by block parity)
-          const long long vi = (long long)(b * p.Hq + g * p.G + hh) * p.N + i * kBM;
           float* sv = svec + (blk & 1) * 2 * kBM;
-          {
-            const int qq = et & (kBM - 1);
-            const bool ok = i * kBM + qq < p.N;
-            if (et < kBM) sv[qq] = ok ? __ldg(p.lse + vi + qq) * 1.4426950408889634f : 0.f;
-            else sv[kBM + qq] = ok ? __ldg(p.dvec + vi + qq) : 0.f;
-            ptx::named_bar_sync(1, 256);
+          sv[et < kBM ? qq : kBM + qq] = staged;
+          ptx::named_bar_sync(1, 256);
+          {  // prefetch the next block's value
+            const bool last_i = i + 1 == p.nblk;
+            if (!last_i || hh + 1 < p.G) staged = stage_load(last_i ? hh + 1 : hh, last_i ? i0 : i + 1);
           }
           ++blk;
           // visible queries of this key: q >= k (causal), q < N; local query index
