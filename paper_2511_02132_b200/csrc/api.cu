@@ -509,13 +509,13 @@ int launch_bwd_t(DevState& st, const CUtensorMap& tq, const CUtensorMap& tdo, co
   const int idx = (D == 128 ? 0 : 2) + (kCausal ? 1 : 0);
   auto* kq = bwd::attn_bwd_dq_kernel<D, kCausal>;
   auto* kkv = bwd::attn_bwd_dkdv_kernel<D, kCausal>;
-  const int smem = bwd::BCfg<D>::kSmemBytes, smem_kv = bwd::BCfg<D>::kSmemBytesKV;
+  const int smem_kv = bwd::BCfg<D>::kSmemBytesKV;
   if (!st.battr_done[idx]) {
-    ATTN_CUDA(cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    ATTN_CUDA(cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, bwd::BCfg<D>::kSmemBytesQ));
     ATTN_CUDA(cudaFuncSetAttribute(kkv, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_kv));
     st.battr_done[idx] = true;
   }
-  kq<<<grid_q, bwd::kThreadsKV, smem, s>>>(tq, tdo, tk, tv, pq);
+  kq<<<grid_q, bwd::kThreadsKV, bwd::BCfg<D>::kSmemBytesQ, s>>>(tq, tdo, tk, tv, pq);
   ATTN_CUDA(cudaGetLastError());
   kkv<<<grid_kv, bwd::kThreadsKV, smem_kv, s>>>(tq, tdo, tk, tv, pkv);
   ATTN_CUDA(cudaGetLastError());

@@ -47,8 +47,11 @@ struct BCfg {
   static constexpr int kOffA = 3072;          // resident pair (dQ: Q, dO;  dKdV: K, V)
   static constexpr int kOffRing = kOffA + 2 * kTile;  // ring of streamed pairs (dQ: K, V;  dKdV: Q, dO)
   static constexpr int kOffPT = kOffRing + kStages * 2 * kTile;  // dKdV: P^T, 128 x 128 bf16 (SW128 K-major)
-  static constexpr int kSmemBytes = kOffPT;                      // dQ kernel
   static constexpr int kSmemBytesKV = kOffPT + kBM * kBM * 2;    // dK/dV kernel
+  // dQ kernel: Q / dO go to TMEM, so its ring holds single K or V tiles
+  static constexpr int kQSlots = 5;
+  static constexpr int kSmemBytesQ = kOffRing + kQSlots * kTile;
+  static_assert(kSmemBytesQ <= 232448, "dQ SMEM over the 227 KB opt-in limit");
   static_assert(kSmemBytesKV <= 232448, "dK/dV SMEM over the 227 KB opt-in limit");
 };
 
@@ -71,7 +74,7 @@ struct __align__(16) BCtrl {
   uint64_t sched_full[kSchedRing];
   uint64_t sched_empty[kSchedRing];
   uint64_t a_full, a_empty;             // resident pair
-  uint64_t ring_full[4], ring_empty[4]; // streamed pairs
+  uint64_t ring_full[5], ring_empty[5]; // streamed pairs (dKdV) / single tiles (dQ)
   uint64_t s_ready, p_ready, o_ready;
   uint64_t dp_ready, ds_ready;          // dP in TMEM, dS stored (bf16, TMEM)
   uint64_t q_ready;                     // dQ: Q and dO copied into TMEM
@@ -171,7 +174,7 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
   uint8_t* smem = smem_raw;
   if (ptx::smem_u32(smem_raw) & 1023) __trap();  // layout relies on a 1024-B aligned base
   uint8_t* sq = smem + C::kOffA;             // Q tile, then dO tile
-  uint8_t* ring = smem + C::kOffRing;        // stage s: K at 2s, V at 2s+1
+  uint8_t* ring = smem + C::kOffRing;        // kQSlots single-tile slots: K_0, V_0, K_1, V_1, ...
   BCtrl* ctrl = reinterpret_cast<BCtrl*>(smem + C::kOffCtrl);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // TMEM: S [0,128), dP [128,256), dQ [256, 256+D), Q [384, 384+D/2), dO [448, 448+D/2)
@@ -187,7 +190,7 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
     }
     ptx::mbar_init(&ctrl->a_full, 1);
     ptx::mbar_init(&ctrl->a_empty, kEw);   // Q / dO SMEM copied into TMEM
-    for (int i = 0; i < C::kStages; ++i) {
+    for (int i = 0; i < C::kQSlots; ++i) {
       ptx::mbar_init(&ctrl->ring_full[i], 1);
       ptx::mbar_init(&ctrl->ring_empty[i], 1);
     }
@@ -230,30 +233,39 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
         }
         const int n = dq_nblocks<kCausal>(i, p.nblk);
         for (int j = 0; j < n; ++j) {
-          ptx::mbar_wait(&ctrl->ring_empty[stage], r_phase ^ 1);
-          ptx::mbar_arrive_expect_tx(&ctrl->ring_full[stage], 2 * C::kTile);
-          uint8_t* dst = ring + stage * 2 * C::kTile;
 #pragma unroll
-          for (int c = 0; c < C::kChunks; ++c) {
-            ptx::tma_load_3d(dst + c * kBM * 128, &tm_k, &ctrl->ring_full[stage], c * 64, j * kBM, kvbh, pol_kv);
-            ptx::tma_load_3d(dst + C::kTile + c * kBM * 128, &tm_v, &ctrl->ring_full[stage], c * 64, j * kBM, kvbh,
-                             pol_kv);
+          for (int which = 0; which < 2; ++which) {  // K_j, then V_j, one slot each
+            ptx::mbar_wait(&ctrl->ring_empty[stage], r_phase ^ 1);
+            ptx::mbar_arrive_expect_tx(&ctrl->ring_full[stage], C::kTile);
+            uint8_t* dst = ring + stage * C::kTile;
+#pragma unroll
+            for (int c = 0; c < C::kChunks; ++c)
+              ptx::tma_load_3d(dst + c * kBM * 128, which == 0 ? (const void*)&tm_k : (const void*)&tm_v,
+                               &ctrl->ring_full[stage], c * 64, j * kBM, kvbh, pol_kv);
+            if (++stage == C::kQSlots) { stage = 0; r_phase ^= 1; }
           }
-          if (++stage == C::kStages) { stage = 0; r_phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
     // Per block j the tensor pipe runs  S(j+1) . dQ(j) . dP(j+1):  S(j+1) is
     // issued as soon as the elementwise warps have read S(j) (P stays in their
-    // registers), so the exps of block j+1 overlap dQ(j) and dP(j+1).
+    // registers), so the exps of block j+1 overlap dQ(j) and dP(j+1).  Ring
+    // slots are taken in the producer's order (K_j+1, then V_j+1); V_j is
+    // released after dP(j), K_j after dQ(j).
     BSchedReader sr;
     constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(kBM, kBM, 0, 0);  // S, dP: K-major A and B
     constexpr uint32_t idesc_q = ptx::idesc_bf16_f32(kBM, D, 0, 1);    // dQ: A = dS (TMEM), B = K MN-major
     const uint64_t dr0 = ptx::smem_desc_sw128(ptx::smem_u32(ring), 16, 1024);
     const uint64_t drm0 = ptx::smem_desc_sw128(ptx::smem_u32(ring), kBM * 128, 1024);
     uint32_t a_phase = 0, r_phase = 0, p_phase = 0;
-    int stage = 0;
+    int slot = 0;
+    auto take = [&]() {
+      const int sl = slot;
+      ptx::mbar_wait(&ctrl->ring_full[sl], r_phase);
+      if (++slot == C::kQSlots) { slot = 0; r_phase ^= 1; }
+      return sl;
+    };
     auto ts_mma = [&](uint32_t d_col, uint32_t a_col, uint64_t b) {  // [128 x 128] = A[128 x D] (TMEM) B[128 x D]^T
 #pragma unroll
       for (int k = 0; k < D / 16; ++k) {
@@ -261,39 +273,34 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
         ptx::mma_ts(tmem + d_col, tmem + a_col + k * 8, b + off, idesc_s, k > 0 ? 1u : 0u);
       }
     };
+    auto kmaj = [&](int sl) { return dr0 + (uint64_t)((sl * C::kTile) >> 4); };
     while (true) {
       const int4 e = sr.next(ctrl);
       if (!e.w) break;
       const int n = dq_nblocks<kCausal>(e.z, p.nblk);
       ptx::mbar_wait(&ctrl->q_ready, a_phase);
       a_phase ^= 1;
-      int st = stage;
-      ptx::mbar_wait(&ctrl->ring_full[st], r_phase);
+      int sK = take();
+      const int sV0 = take();
       ptx::tc_fence_after();
       if (ptx::elect_one_sync()) {
-        const uint64_t kd = dr0 + (uint64_t)((st * 2 * C::kTile) >> 4);
-        ts_mma(kColS, kColQ, kd);                                   // S  = Q  K_0^T
+        ts_mma(kColS, kColQ, kmaj(sK));                             // S  = Q  K_0^T
         ptx::mma_commit(&ctrl->s_ready);
-        ts_mma(kColDP, kColDO, kd + (uint64_t)(C::kTile >> 4));     // dP = dO V_0^T
+        ts_mma(kColDP, kColDO, kmaj(sV0));                          // dP = dO V_0^T
         ptx::mma_commit(&ctrl->dp_ready);
+        ptx::mma_commit(&ctrl->ring_empty[sV0]);
       }
       __syncwarp();
       for (int j = 0; j < n; ++j) {
-        const int cur = st;
         const bool nxt = j + 1 < n;
-        int nst = cur, nph = r_phase;
-        if (nxt) {
-          nst = cur + 1 == C::kStages ? 0 : cur + 1;
-          nph = cur + 1 == C::kStages ? r_phase ^ 1 : r_phase;
-        }
-        const uint64_t kd = dr0 + (uint64_t)((nst * 2 * C::kTile) >> 4);
         ptx::mbar_wait(&ctrl->p_ready, p_phase);   // S(j) read
         ptx::tc_fence_after();
+        int sK1 = sK;
         if (nxt) {
-          ptx::mbar_wait(&ctrl->ring_full[nst], nph);
+          sK1 = take();
           ptx::tc_fence_after();
           if (ptx::elect_one_sync()) {
-            ts_mma(kColS, kColQ, kd);               // S(j+1)
+            ts_mma(kColS, kColQ, kmaj(sK1));        // S(j+1)
             ptx::mma_commit(&ctrl->s_ready);
           }
           __syncwarp();
@@ -301,29 +308,30 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
         ptx::mbar_wait(&ctrl->ds_ready, p_phase);
         p_phase ^= 1;
         ptx::tc_fence_after();
+        int sV1 = -1;
+        if (nxt) sV1 = take();
+        ptx::tc_fence_after();
         if (ptx::elect_one_sync()) {
           // dQ += dS K_j: A = dS (bf16 in TMEM over dP; queries' keys 0-63 in
           // columns [0,32), keys 64-127 in [64,96) of the region), B = K_j as
           // [keys x D] (MN-major)
-          const uint64_t km = drm0 + (uint64_t)((cur * 2 * C::kTile) >> 4);
+          const uint64_t km = drm0 + (uint64_t)((sK * C::kTile) >> 4);
 #pragma unroll
           for (int k = 0; k < kBM / 16; ++k)
             ptx::mma_ts(tmem + kColDQ, tmem + kColDP + k * 8 + (k >= 4 ? 32 : 0),
                         km + (uint64_t)((k * 16 * 128) >> 4), idesc_q, (j > 0 || k > 0) ? 1u : 0u);
-          ptx::mma_commit(&ctrl->ring_empty[cur]);
+          ptx::mma_commit(&ctrl->ring_empty[sK]);
           if (nxt) {
-            ts_mma(kColDP, kColDO, kd + (uint64_t)(C::kTile >> 4));  // dP(j+1)
+            ts_mma(kColDP, kColDO, kmaj(sV1));      // dP(j+1)
             ptx::mma_commit(&ctrl->dp_ready);
+            ptx::mma_commit(&ctrl->ring_empty[sV1]);
           } else {
             ptx::mma_commit(&ctrl->o_ready);
           }
         }
         __syncwarp();
-        st = nst;
-        r_phase = nph;
+        sK = sK1;
       }
-      stage = st + 1 == C::kStages ? 0 : st + 1;
-      if (st + 1 == C::kStages) r_phase ^= 1;
     }
   } else if (warp == 2) {
     if (lane == 0) bwd_scheduler(p, ctrl, p.Hq);
