@@ -568,6 +568,7 @@ int bwd_impl(const void* q, const void* k, const void* v, const void* o, const v
   pq.dk = reinterpret_cast<__nv_bfloat16*>(dk);
   pq.dv = reinterpret_cast<__nv_bfloat16*>(dv);
   pq.domain_of_smid = st.d_domain;
+  pq.dbg = reinterpret_cast<long long*>(st.trace);  // ATTN_BWD_TIMELINE builds only
   pq.n_smid = ATTN_MAX_SMID;
   bwd::BwdParams pkv = pq;
   // dQ units: (b, query head, query block); dK/dV units: (b, KV group, key block)

@@ -68,6 +68,7 @@ struct BwdParams {
   int* counters;
   const signed char* domain_of_smid;
   int n_smid;
+  long long* dbg;      // -D ATTN_BWD_TIMELINE: per-block stamps of CTA 0 (the trace buffer), else unused
 };
 
 struct __align__(16) BCtrl {
@@ -274,10 +275,19 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
       }
     };
     auto kmaj = [&](int sl) { return dr0 + (uint64_t)((sl * C::kTile) >> 4); };
+#ifdef ATTN_BWD_TIMELINE
+    int unit_no = 0;
+#define BWD_STAMP(j, i) if (p.dbg && blockIdx.x == 0 && lane == 0 && unit_no == 1 && (j) < 64) p.dbg[(j) * 16 + (i)] = clock64();
+#else
+#define BWD_STAMP(j, i)
+#endif
     while (true) {
       const int4 e = sr.next(ctrl);
       if (!e.w) break;
       const int n = dq_nblocks<kCausal>(e.z, p.nblk);
+#ifdef ATTN_BWD_TIMELINE
+      ++unit_no;
+#endif
       ptx::mbar_wait(&ctrl->q_ready, a_phase);
       a_phase ^= 1;
       int sK = take();
@@ -294,6 +304,7 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
       for (int j = 0; j < n; ++j) {
         const bool nxt = j + 1 < n;
         ptx::mbar_wait(&ctrl->p_ready, p_phase);   // S(j) read
+        BWD_STAMP(j, 0);
         ptx::tc_fence_after();
         int sK1 = sK;
         if (nxt) {
@@ -305,7 +316,9 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
           }
           __syncwarp();
         }
+        BWD_STAMP(j, 1);
         ptx::mbar_wait(&ctrl->ds_ready, p_phase);
+        BWD_STAMP(j, 2);
         p_phase ^= 1;
         ptx::tc_fence_after();
         int sV1 = -1;
@@ -330,9 +343,11 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
           }
         }
         __syncwarp();
+        BWD_STAMP(j, 3);
         sK = sK1;
       }
     }
+#undef BWD_STAMP
   } else if (warp == 2) {
     if (lane == 0) bwd_scheduler(p, ctrl, p.Hq);
   } else if (warp >= 4) {
@@ -344,6 +359,9 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
     const float c = p.scale_log2;
     BSchedReader sr;
     uint32_t s_phase = 0, o_phase = 0, a_phase = 0;
+#ifdef ATTN_BWD_TIMELINE
+    int unit_no = 0;
+#endif
     while (true) {
       const int4 e = sr.next(ctrl);
       if (!e.w) break;
@@ -379,6 +397,13 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
       const float lse2 = valid ? p.lse[ridx] * 1.4426950408889634f : 0.f;
       const float dd = valid ? p.dvec[ridx] : 0.f;
       const int n = dq_nblocks<kCausal>(i, p.nblk);
+#ifdef ATTN_BWD_TIMELINE
+      ++unit_no;
+#define BWD_ESTAMP(j, i) if (p.dbg && blockIdx.x == 0 && lane == 0 && quarter == 0 && unit_no == 1 && (j) < 64) \
+    p.dbg[(j) * 16 + 4 + 5 * half + (i)] = clock64();
+#else
+#define BWD_ESTAMP(j, i)
+#endif
       for (int j = 0; j < n; ++j) {
         // visible keys of this row in block j: k <= lim (causal diagonal, ragged tail)
         int lim = kBM - 1;
@@ -387,21 +412,31 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
         if (!valid) lim = -1;
         float pv[64];
         ptx::mbar_wait(&ctrl->s_ready, s_phase);
+        BWD_ESTAMP(j, 0);
         ptx::tc_fence_after();
-#pragma unroll
-        for (int cc = 0; cc < 64; cc += 32) {
-          uint32_t sr_[32];
-          ptx::tmem_ld32(trow + kColS + k0c + cc, sr_);
-#pragma unroll
-          for (int k = 0; k < 32; ++k) {
-            const float pe = ptx::ex2(fmaf(__uint_as_float(sr_[k]), c, -lse2));
-            pv[cc + k] = (k0c + cc + k <= lim) ? pe : 0.f;
-          }
-        }
+        // S -> registers, then release the S region (S(j+1) is issued at once)
+        ptx::tmem_ld32(trow + kColS + k0c, reinterpret_cast<uint32_t*>(pv));
+        ptx::tmem_ld32(trow + kColS + k0c + 32, reinterpret_cast<uint32_t*>(pv) + 32);
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&ctrl->p_ready);
+        BWD_ESTAMP(j, 1);
+        // masking (causal diagonal, ragged tail, rows past N) only where some
+        // lane of the warp needs it: a warp-uniform branch, no per-element
+        // compare + select on the common path
+        if (__any_sync(0xffffffffu, lim < k0c + 63)) {
+#pragma unroll
+          for (int k = 0; k < 64; ++k) {
+            const float pe = ptx::ex2(fmaf(pv[k], c, -lse2));
+            pv[k] = (k0c + k <= lim) ? pe : 0.f;
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < 64; ++k) pv[k] = ptx::ex2(fmaf(pv[k], c, -lse2));
+        }
+        BWD_ESTAMP(j, 2);
         ptx::mbar_wait(&ctrl->dp_ready, s_phase);
+        BWD_ESTAMP(j, 3);
         s_phase ^= 1;
         ptx::tc_fence_after();
 #pragma unroll
@@ -419,7 +454,9 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&ctrl->ds_ready);
+        BWD_ESTAMP(j, 4);
       }
+#undef BWD_ESTAMP
       ptx::mbar_wait(&ctrl->o_ready, o_phase);
       o_phase ^= 1;
       ptx::tc_fence_after();
@@ -686,15 +723,27 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
           ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&ctrl->s_free);   // S^T region may be overwritten
+          // masking only where some lane needs it (warp-uniform branch)
+          if (__any_sync(0xffffffffu, qlo > q0c || qhi < q0c + 63)) {
 #pragma unroll
-          for (int k = 0; k < 64; k += 4) {
-            const float4 l4 = *reinterpret_cast<const float4*>(sv + q0c + k);
-            const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+            for (int k = 0; k < 64; k += 4) {
+              const float4 l4 = *reinterpret_cast<const float4*>(sv + q0c + k);
+              const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int q = q0c + k + u;
-              const float pe = ptx::ex2(fmaf(pv[k + u], c, -lv[u]));
-              pv[k + u] = (q >= qlo && q <= qhi) ? pe : 0.f;
+              for (int u = 0; u < 4; ++u) {
+                const int q = q0c + k + u;
+                const float pe = ptx::ex2(fmaf(pv[k + u], c, -lv[u]));
+                pv[k + u] = (q >= qlo && q <= qhi) ? pe : 0.f;
+              }
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < 64; k += 4) {
+              const float4 l4 = *reinterpret_cast<const float4*>(sv + q0c + k);
+              pv[k] = ptx::ex2(fmaf(pv[k], c, -l4.x));
+              pv[k + 1] = ptx::ex2(fmaf(pv[k + 1], c, -l4.y));
+              pv[k + 2] = ptx::ex2(fmaf(pv[k + 2], c, -l4.z));
+              pv[k + 3] = ptx::ex2(fmaf(pv[k + 3], c, -l4.w));
             }
           }
           // P^T -> SMEM (SW128 K-major: key row krow, 16-B unit u at (u ^ (krow & 7)))
