@@ -32,6 +32,18 @@ namespace attn {
 namespace bwd {
 
 constexpr int kBM = 128;       // rows of a query block / keys of a key block
+
+// Every ATTN_BWD_EMU_PERIOD-th exp2 of the P phases runs as a polynomial on the
+// FMA pipe instead of MUFU (0 = all on MUFU); see ptx::ex2_poly.
+#ifndef ATTN_BWD_EMU_PERIOD
+#define ATTN_BWD_EMU_PERIOD 8
+#endif
+// k: the element's index in a fully unrolled loop (the test folds away).
+__device__ __forceinline__ float bwd_ex2(float x, int k) {
+  constexpr int P = ATTN_BWD_EMU_PERIOD > 0 ? ATTN_BWD_EMU_PERIOD : 1;
+  if (ATTN_BWD_EMU_PERIOD > 0 && k % P == P - 1) return ptx::ex2_poly(x);
+  return ptx::ex2(x);
+}
 constexpr int kThreadsKV = 384;  // warps 0 TMA, 1 MMA, 2 scheduler + TMEM, 3 idle, 4-11 elementwise (two column halves)
 
 template <int D>
@@ -427,12 +439,12 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
         if (__any_sync(0xffffffffu, lim < k0c + 63)) {
 #pragma unroll
           for (int k = 0; k < 64; ++k) {
-            const float pe = ptx::ex2(fmaf(pv[k], c, -lse2));
+            const float pe = bwd_ex2(fmaf(pv[k], c, -lse2), k);
             pv[k] = (k0c + k <= lim) ? pe : 0.f;
           }
         } else {
 #pragma unroll
-          for (int k = 0; k < 64; ++k) pv[k] = ptx::ex2(fmaf(pv[k], c, -lse2));
+          for (int k = 0; k < 64; ++k) pv[k] = bwd_ex2(fmaf(pv[k], c, -lse2), k);
         }
         BWD_ESTAMP(j, 2);
         ptx::mbar_wait(&ctrl->dp_ready, s_phase);
@@ -732,7 +744,7 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
                 const int q = q0c + k + u;
-                const float pe = ptx::ex2(fmaf(pv[k + u], c, -lv[u]));
+                const float pe = bwd_ex2(fmaf(pv[k + u], c, -lv[u]), k + u);
                 pv[k + u] = (q >= qlo && q <= qhi) ? pe : 0.f;
               }
             }
@@ -740,10 +752,10 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
 #pragma unroll
             for (int k = 0; k < 64; k += 4) {
               const float4 l4 = *reinterpret_cast<const float4*>(sv + q0c + k);
-              pv[k] = ptx::ex2(fmaf(pv[k], c, -l4.x));
-              pv[k + 1] = ptx::ex2(fmaf(pv[k + 1], c, -l4.y));
-              pv[k + 2] = ptx::ex2(fmaf(pv[k + 2], c, -l4.z));
-              pv[k + 3] = ptx::ex2(fmaf(pv[k + 3], c, -l4.w));
+              pv[k] = bwd_ex2(fmaf(pv[k], c, -l4.x), k);
+              pv[k + 1] = bwd_ex2(fmaf(pv[k + 1], c, -l4.y), k + 1);
+              pv[k + 2] = bwd_ex2(fmaf(pv[k + 2], c, -l4.z), k + 2);
+              pv[k + 3] = bwd_ex2(fmaf(pv[k + 3], c, -l4.w), k + 3);
             }
           }
           // P^T -> SMEM (SW128 K-major: key row krow, 16-B unit u at (u ^ (krow & 7)))
