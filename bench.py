@@ -33,6 +33,8 @@ WORKLOADS = {
     "C3": (1, 128, 128, 32768, 128, True, "weak"),
     "C4": (2, 64, 8, 16384, 128, True, "weak"),
     "C5": (1, 128, 128, 131072, 128, True, "strong"),
+    # NEXT-2: DeepSeek-V3 prefill (Table 2: MHA 128/128, d = 56; fig:dsmhaperf N 2K-128K)
+    "C6": (1, 128, 128, 32768, 56, True, "weak"),
 }
 METRIC = "attention fwd TFLOP/s (% of bf16 peak) and L2 hit rate by mapping, 1/2/4/8 B200"
 MAPS = ("block_first", "head_first", "swizzled_head_first", "swizzled_block_first")

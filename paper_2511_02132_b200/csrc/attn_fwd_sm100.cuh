@@ -66,6 +66,14 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units; see DESIGN.md "fix-up"
 #endif
 
 constexpr int kEmuPeriod = ATTN_EMU_PERIOD;  // every kEmuPeriod-th exp2 pair runs on the FMA pipe (0: none)
+// Head dim <= 64: half the tensor work per exp, so the exps bound the kernel
+// (MUFU alone would cap it near 57% of the tensor peak) and a larger share
+// goes to the FMA-pipe polynomial.
+#ifndef ATTN_EMU_PERIOD_D64
+#define ATTN_EMU_PERIOD_D64 8
+#endif
+template <int D>
+constexpr int emu_period() { return D <= 64 ? ATTN_EMU_PERIOD_D64 : kEmuPeriod; }
 // Register split (setmaxnreg).  The CTA's register pool is what the launch
 // allocated: kThreads * kInitRegs (ptxas caps a thread at 65536 / kThreads,
 // rounded down to a multiple of 8).  Warps 0-3 release registers that the
@@ -751,7 +759,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = h * kCols / 2; k < (h + 1) * kCols / 2; k += 2) {
             const float2 x = ptx::ffma2(make_float2(__uint_as_float(r[k]), __uint_as_float(r[k + 1])), c, neg);
             float2 pr;
-            if (kEmuPeriod > 0 && ((k >> 1) % (kEmuPeriod > 0 ? kEmuPeriod : 1)) == kEmuPeriod - 1) {
+            constexpr int kEP = emu_period<D>();
+            if (kEP > 0 && ((k >> 1) % (kEP > 0 ? kEP : 1)) == kEP - 1) {
               pr = ptx::ex2_poly2(x);
             } else {
 #if ATTN_EXP_F16X2

@@ -9,7 +9,8 @@ sys.path.insert(0, ".")
 from paper_2511_02132_b200 import attn_fwd, attn_topology, synth
 
 CFG = {"C2": (1, 32, 32, 8192, 128, False), "C3": (1, 128, 128, 32768, 128, True),
-       "C4": (2, 64, 8, 16384, 128, True), "C5": (1, 128, 128, 131072, 128, True)}
+       "C4": (2, 64, 8, 16384, 128, True), "C5": (1, 128, 128, 131072, 128, True),
+       "C6": (1, 128, 128, 32768, 56, True)}
 ap = argparse.ArgumentParser()
 ap.add_argument("--configs", default="C2,C3,C4")
 ap.add_argument("--reps", type=int, default=10)
