@@ -156,15 +156,15 @@ __device__ __forceinline__ void unit_blocks(int u, int nblk, int& n0, int& n1) {
 // Consumer side of the scheduler ring.  kCl == 2 (CTA-pair clusters): the
 // entries are written by the leader CTA's scheduler into both CTAs, and every
 // consumer of both CTAs releases the slot on the LEADER's sched_empty.
-template <int kCl>
+template <int kCl, class CT = Ctrl>
 struct SchedReader {
   int stage = 0;
   uint32_t phase = 0;
-  __device__ __forceinline__ void release(Ctrl* c, int st) {
+  __device__ __forceinline__ void release(CT* c, int st) {
     if constexpr (kCl == 1) ptx::mbar_arrive(&c->sched_empty[st]);
     else ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&c->sched_empty[st]), 0));
   }
-  __device__ __forceinline__ int4 next(Ctrl* c, bool arrive) {
+  __device__ __forceinline__ int4 next(CT* c, bool arrive) {
     if constexpr (kCl == 1) ptx::mbar_wait(&c->sched_full[stage], phase);
     else ptx::mbar_wait_cluster(&c->sched_full[stage], phase);
     const volatile int* ve = reinterpret_cast<const volatile int*>(&c->entry[stage]);
@@ -173,7 +173,7 @@ struct SchedReader {
     if (++stage == kSchedRing) { stage = 0; phase ^= 1; }
     return e;
   }
-  __device__ __forceinline__ void release_prev(Ctrl* c) { release(c, (stage + kSchedRing - 1) % kSchedRing); }
+  __device__ __forceinline__ void release_prev(CT* c) { release(c, (stage + kSchedRing - 1) % kSchedRing); }
 };
 
 // This CTA's (head, unit) of a scheduler entry (b, h, u, w).  kCl == 1: (h, u).
@@ -209,6 +209,76 @@ __device__ __forceinline__ int pair_kv_blocks(const int4& e, const KernelParams&
   if (p.pair_heads) return unit_kv_blocks<kCausal>(e.z, p.nblk);
   return max(unit_kv_blocks<kCausal>(2 * e.z, p.nblk),
              unit_kv_blocks<kCausal>(2 * e.z + 1 < p.U ? 2 * e.z + 1 : -1, p.nblk));
+}
+
+// The scheduler warp (lane 0): pop this SM's die queue (or the shared one),
+// steal from the others when it runs dry, and broadcast (b, h, unit) to the
+// CTA's consumers through the 2-entry SMEM ring; kCl == 2: the leader CTA
+// serves both CTAs of the pair.
+template <int kCl, class CT>
+__device__ __forceinline__ void run_scheduler(const KernelParams& p, CT* ctrl) {
+  const int sm = (int)ptx::smid();
+  int dom = (sm < p.n_smid) ? (int)p.domain_of_smid[sm] : 0;
+  if (dom < 0) dom = 0;
+  const int nq = p.sched.n_queues;
+  const int q0 = (nq > 1) ? p.sched.queue_of_domain[dom] : 0;
+  uint32_t exhausted = 0;
+  int stage = 0;
+  uint32_t phase = 0;
+  int seq = 0;
+  while (true) {
+    int b = 0, h = 0, u = 0, qi = -1, stolen = 0;
+    for (int t = 0; t < nq; ++t) {
+      if (t > 0 && !p.sched.steal) break;
+      const int qq = (q0 + t) % nq;
+      if (exhausted & (1u << qq)) continue;
+      const int pos = atomicAdd(&p.counters[qq * 32], 1);
+      if (pos < p.sched.q[qq].len) {
+        decode_unit(p.sched.q[qq], pos, p.Hsched, p.Usched, b, h, u);
+        if (p.sched.descending) u = p.Usched - 1 - u;
+        qi = qq;
+        stolen = t > 0;
+        break;
+      }
+      exhausted |= 1u << qq;
+    }
+    if constexpr (kCl == 1) {
+      ptx::mbar_wait(&ctrl->sched_empty[stage], phase ^ 1);
+      ctrl->entry[stage] = make_int4(b, h, u, qi >= 0 ? 1 : 0);
+      ptx::mbar_arrive(&ctrl->sched_full[stage]);
+    } else {
+      // both CTAs' consumers released the slot on this (leader) CTA's barrier;
+      // w packs valid | queue << 1 | stolen << 7 for the peers' trace records
+      ptx::mbar_wait_cluster(&ctrl->sched_empty[stage], phase ^ 1);
+      const int4 ent = make_int4(b, h, u, qi >= 0 ? (1 | (qi << 1) | (stolen << 7)) : 0);
+      ctrl->entry[stage] = ent;
+      ptx::st_cluster_v4(ptx::mapa_shared(ptx::smem_u32(&ctrl->entry[stage]), 1), ent);
+      ptx::mbar_arrive(&ctrl->sched_full[stage]);
+      ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&ctrl->sched_full[stage]), 1));
+    }
+    if (qi < 0) break;
+#ifndef ATTN_PROFILE_WAITS
+    if (kCl == 1 && p.trace) {
+      const long long id = ((long long)b * p.Hq + h) * p.U + u;
+      if (id < p.trace_cap) {
+        attn_trace_rec_t r;
+        r.b = b; r.h = h; r.unit = u; r.smid = sm; r.domain = dom; r.queue = qi;
+        r.stolen = stolen; r.seq = seq; r.t_pop_ns = ptx::globaltimer();
+        p.trace[id] = r;
+      }
+    }
+#endif
+    ++seq;
+    if (++stage == kSchedRing) { stage = 0; phase ^= 1; }
+  }
+  // Self-resetting counters: the last CTA to finish popping zeroes the
+  // queue counters for the next launch on this slot (no host memset).
+  __threadfence();
+  if (atomicAdd(&p.counters[kDoneCounter], 1) == (int)gridDim.x / kCl - 1) {
+    for (int q = 0; q < nq; ++q) atomicExch(&p.counters[q * 32], 0);
+    atomicExch(&p.counters[kDoneCounter], 0);
+    __threadfence();
+  }
 }
 
 // kCl == 2: CTA-pair clusters (NEXT-4).  The pair works on the two halves of
@@ -560,70 +630,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 2) {
     // --------------------------------------------------------------- scheduler
     if (ATTN_SETMAXNREG) ptx::setmaxnreg_dec<kOtherRegs>();
-    if (lane == 0 && crank == 0) {  // clusters: the leader CTA schedules for the pair
-      const int sm = (int)ptx::smid();
-      int dom = (sm < p.n_smid) ? (int)p.domain_of_smid[sm] : 0;
-      if (dom < 0) dom = 0;
-      const int nq = p.sched.n_queues;
-      const int q0 = (nq > 1) ? p.sched.queue_of_domain[dom] : 0;
-      uint32_t exhausted = 0;
-      int stage = 0;
-      uint32_t phase = 0;
-      int seq = 0;
-      while (true) {
-        int b = 0, h = 0, u = 0, qi = -1, stolen = 0;
-        for (int t = 0; t < nq; ++t) {
-          if (t > 0 && !p.sched.steal) break;
-          const int qq = (q0 + t) % nq;
-          if (exhausted & (1u << qq)) continue;
-          const int pos = atomicAdd(&p.counters[qq * 32], 1);
-          if (pos < p.sched.q[qq].len) {
-            decode_unit(p.sched.q[qq], pos, p.Hsched, p.Usched, b, h, u);
-            if (p.sched.descending) u = p.Usched - 1 - u;
-            qi = qq;
-            stolen = t > 0;
-            break;
-          }
-          exhausted |= 1u << qq;
-        }
-        if constexpr (kCl == 1) {
-          ptx::mbar_wait(&ctrl->sched_empty[stage], phase ^ 1);
-          ctrl->entry[stage] = make_int4(b, h, u, qi >= 0 ? 1 : 0);
-          ptx::mbar_arrive(&ctrl->sched_full[stage]);
-        } else {
-          // both CTAs' consumers released the slot on this (leader) CTA's barrier;
-          // w packs valid | queue << 1 | stolen << 7 for the peers' trace records
-          ptx::mbar_wait_cluster(&ctrl->sched_empty[stage], phase ^ 1);
-          const int4 ent = make_int4(b, h, u, qi >= 0 ? (1 | (qi << 1) | (stolen << 7)) : 0);
-          ctrl->entry[stage] = ent;
-          ptx::st_cluster_v4(ptx::mapa_shared(ptx::smem_u32(&ctrl->entry[stage]), 1), ent);
-          ptx::mbar_arrive(&ctrl->sched_full[stage]);
-          ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&ctrl->sched_full[stage]), 1));
-        }
-        if (qi < 0) break;
-#ifndef ATTN_PROFILE_WAITS
-        if (kCl == 1 && p.trace) {
-          const long long id = ((long long)b * p.Hq + h) * p.U + u;
-          if (id < p.trace_cap) {
-            attn_trace_rec_t r;
-            r.b = b; r.h = h; r.unit = u; r.smid = sm; r.domain = dom; r.queue = qi;
-            r.stolen = stolen; r.seq = seq; r.t_pop_ns = ptx::globaltimer();
-            p.trace[id] = r;
-          }
-        }
-#endif
-        ++seq;
-        if (++stage == kSchedRing) { stage = 0; phase ^= 1; }
-      }
-      // Self-resetting counters: the last CTA to finish popping zeroes the
-      // queue counters for the next launch on this slot (no host memset).
-      __threadfence();
-      if (atomicAdd(&p.counters[kDoneCounter], 1) == (int)gridDim.x / kCl - 1) {
-        for (int q = 0; q < nq; ++q) atomicExch(&p.counters[q * 32], 0);
-        atomicExch(&p.counters[kDoneCounter], 0);
-        __threadfence();
-      }
-    }
+    if (lane == 0 && crank == 0) run_scheduler<kCl>(p, ctrl);  // clusters: the leader schedules for the pair
   } else if (warp >= 4) {
     // ------------------------------------------------ softmax / fix-up / epilogue
     if (ATTN_SETMAXNREG) ptx::setmaxnreg_inc<kSoftmaxRegs>();
