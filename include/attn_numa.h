@@ -1,5 +1,6 @@
 /*
- * attn_numa.h -- C-ABI boundary of the B200 attention-forward hot path.
+ * attn_numa.h -- C-ABI boundary of the B200 attention hot path (forward,
+ * and the backward of NEXT-3).
  *
  * The library computes the FlashAttention-2-style forward pass of
  * PAPER.md eq:fa (lines 149-155),
@@ -8,7 +9,7 @@
  *
  * for multi-head (Hq == Hkv) and grouped-query (Hkv < Hq) attention
  * (PAPER.md:167), tiled into work units of query-row blocks (PAPER.md:174,
- * fig:fa2), and hands those units to SMs in one of three orders (the
+ * fig:fa2), and hands those units to SMs in one of four orders (the
  * paper's "mappings"):
  *
  *   ATTN_MAP_BLOCK_FIRST          Naive Block-first
@@ -153,8 +154,10 @@ ATTN_API int attn_fwd_lse(const void* q, const void* k, const void* v, void* o, 
  * `mapping` orders the work units exactly as for the forward (dQ: query
  * blocks of a head; dK/dV: key blocks of a KV group).  Three launches:
  * rowsum(dO o O) into library workspace, the dQ kernel, the dK/dV kernel.
- * Same validation and status codes as attn_fwd; gradients must not overlap
- * each other or any input. */
+ * Same validation and status codes as attn_fwd (ATTN_ORDER_DESCENDING
+ * applies; ATTN_CLUSTER_MULTICAST returns ATTN_ERR_UNSUPPORTED: the
+ * backward has no cluster variant); gradients must not overlap each other or
+ * any input. */
 ATTN_API int attn_bwd(const void* q, const void* k, const void* v, const void* o, const void* dout,
                       const float* lse, void* dq, void* dk, void* dv, int B, int Hq, int Hkv, int N, int d,
                       int causal, float scale, int mapping, void* cuda_stream);
