@@ -427,8 +427,7 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
         BWD_ESTAMP(j, 0);
         ptx::tc_fence_after();
         // S -> registers, then release the S region (S(j+1) is issued at once)
-        ptx::tmem_ld32(trow + kColS + k0c, reinterpret_cast<uint32_t*>(pv));
-        ptx::tmem_ld32(trow + kColS + k0c + 32, reinterpret_cast<uint32_t*>(pv) + 32);
+        ptx::tmem_ld64(trow + kColS + k0c, reinterpret_cast<uint32_t*>(pv));   // one wait for 64 columns
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&ctrl->p_ready);
@@ -451,16 +450,18 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
         BWD_ESTAMP(j, 3);
         s_phase ^= 1;
         ptx::tc_fence_after();
+        {
+          uint32_t dp[64];
+          ptx::tmem_ld64(trow + kColDP + k0c, dp);   // one wait for 64 columns
 #pragma unroll
-        for (int cc = 0; cc < 64; cc += 32) {
-          uint32_t dp[32];
-          ptx::tmem_ld32(trow + kColDP + k0c + cc, dp);
-          uint32_t pk[16];
+          for (int cc = 0; cc < 64; cc += 32) {
+            uint32_t pk[16];
 #pragma unroll
-          for (int k = 0; k < 32; k += 2)
-            pk[k >> 1] = ptx::pack_bf16(pv[cc + k] * (__uint_as_float(dp[k]) - dd),
-                                        pv[cc + k + 1] * (__uint_as_float(dp[k + 1]) - dd));
-          ptx::tmem_st16(trow + kColDP + k0c + cc / 2, pk);  // dS (bf16 pairs) over dP columns this half read
+            for (int k = 0; k < 32; k += 2)
+              pk[k >> 1] = ptx::pack_bf16(pv[cc + k] * (__uint_as_float(dp[cc + k]) - dd),
+                                          pv[cc + k + 1] * (__uint_as_float(dp[cc + k + 1]) - dd));
+            ptx::tmem_st16(trow + kColDP + k0c + cc / 2, pk);  // dS (bf16 pairs) over dP columns this half read
+          }
         }
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
@@ -730,8 +731,7 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
           float pv[64];
           ptx::mbar_wait(&ctrl->s_ready, s_phase);
           ptx::tc_fence_after();
-          ptx::tmem_ld32(trow + kColS + q0c, reinterpret_cast<uint32_t*>(pv));
-          ptx::tmem_ld32(trow + kColS + q0c + 32, reinterpret_cast<uint32_t*>(pv) + 32);
+          ptx::tmem_ld64(trow + kColS + q0c, reinterpret_cast<uint32_t*>(pv));   // one wait for 64 columns
           ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&ctrl->s_free);   // S^T region may be overwritten
@@ -776,10 +776,10 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
           ptx::mbar_wait(&ctrl->dp_ready, s_phase);
           s_phase ^= 1;
           ptx::tc_fence_after();
+          uint32_t dp[64];
+          ptx::tmem_ld64(trow + kColDP + q0c, dp);   // one wait for 64 columns
 #pragma unroll
           for (int cc = 0; cc < 64; cc += 32) {
-            uint32_t dp[32];
-            ptx::tmem_ld32(trow + kColDP + q0c + cc, dp);
             uint32_t pd[16];
 #pragma unroll
             for (int k = 0; k < 32; k += 4) {
@@ -787,8 +787,8 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
               const float dvv[4] = {d4.x, d4.y, d4.z, d4.w};
 #pragma unroll
               for (int u = 0; u < 4; u += 2)
-                pd[(k + u) >> 1] = ptx::pack_bf16(pv[cc + k + u] * (__uint_as_float(dp[k + u]) - dvv[u]),
-                                                  pv[cc + k + u + 1] * (__uint_as_float(dp[k + u + 1]) - dvv[u + 1]));
+                pd[(k + u) >> 1] = ptx::pack_bf16(pv[cc + k + u] * (__uint_as_float(dp[cc + k + u]) - dvv[u]),
+                                                  pv[cc + k + u + 1] * (__uint_as_float(dp[cc + k + u + 1]) - dvv[u + 1]));
             }
             ptx::tmem_st16(trow + kColDP + q0c + cc / 2, pd);  // dS^T over consumed dP^T columns
           }
