@@ -49,11 +49,22 @@ constexpr int kBlockN = 128;  // keys per K/V block
 #ifndef ATTN_SPLIT
 #define ATTN_SPLIT 1
 #endif
+// P is published to the MMA warp in kPParts column slices (O += P V starts on
+// the first slice while the softmax computes the rest; 4 slices measured slower).
+#ifndef ATTN_P_PARTS
+#define ATTN_P_PARTS 2
+#endif
+constexpr int kPParts = ATTN_P_PARTS;
+// Speculative block max (experiment, off: measured slower)
+#ifndef ATTN_SPEC_MAX
+#define ATTN_SPEC_MAX 0
+#endif
 // softmax warps per (tile, TMEM lane quarter): each handles kBlockN / kSplit
 // columns of its 32 rows, so two warps share each SMSP's MUFU per tile.
 constexpr int kSplit = ATTN_SPLIT;
 constexpr int kSoftmaxWarps = 8 * kSplit;
 constexpr int kThreads = 128 + 32 * kSoftmaxWarps;
+static_assert(kPParts == 2 || (kPParts == 4 && kSplit == 1), "P slices: 2, or 4 with one warp per row");
 constexpr int kSchedRing = 2;
 constexpr int kTmemCols = 512;
 constexpr int kDoneCounter = kMaxQueues * 32;  // counters[] index of the CTA-done count
@@ -129,7 +140,7 @@ struct __align__(16) Ctrl {
   uint64_t kv_full[8];
   uint64_t kv_empty[8];
   uint64_t s_ready[2];
-  uint64_t p_ready[2][2];   // [tile][half of P]  softmax -> MMA
+  uint64_t p_ready[2][4];   // [tile][slice of P]  softmax -> MMA
   uint64_t o_ready[2];
   int4 entry[kSchedRing];  // (b, h, u, valid)
   uint32_t tmem_base;
@@ -257,7 +268,7 @@ __device__ __forceinline__ void run_scheduler(const KernelParams& p, CT* ctrl) {
       ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&ctrl->sched_full[stage]), 1));
     }
     if (qi < 0) break;
-#ifndef ATTN_PROFILE_WAITS
+#if !defined(ATTN_PROFILE_WAITS) && !defined(ATTN_TIMELINE)
     if (kCl == 1 && p.trace) {
       const long long id = ((long long)b * p.Hq + h) * p.U + u;
       if (id < p.trace_cap) {
@@ -322,8 +333,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&ctrl->s_ready[i], 1);
-      ptx::mbar_init(&ctrl->p_ready[i][0], 4 * kSplit);  // one arrive per softmax warp of the tile
-      ptx::mbar_init(&ctrl->p_ready[i][1], 4 * kSplit);
+      for (int h = 0; h < kPParts; ++h)
+        ptx::mbar_init(&ctrl->p_ready[i][h], 4 * kSplit);  // one arrive per softmax warp of the tile
       ptx::mbar_init(&ctrl->o_ready[i], 1);
     }
     ptx::fence_barrier_init();
@@ -487,15 +498,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
 #endif
     };
-    // O_t += P_t V: K = 128 keys in 8 steps of 16; steps [4h, 4h+4) read the
-    // half h of P, which the softmax publishes separately (p_ready[t][h]).
+    // O_t += P_t V: K = 128 keys in 8 steps of 16; the steps of slice h read
+    // the part of P the softmax publishes separately (p_ready[t][h]).
     auto issue_pv_half = [&](int t, int slot, bool acc, int h) {
       const uint64_t dv = dv0 + (uint64_t)((slot * C::kKVBytes) >> 4);
       const uint32_t d_tmem = tmem + C::col_o(t);
       const uint32_t a_tmem = tmem + C::col_s(t);
 #ifndef ATTN_DEBUG_NO_PV
 #pragma unroll
-      for (int k = 4 * h; k < 4 * h + 4; ++k)
+      for (int k = h * (8 / kPParts); k < (h + 1) * (8 / kPParts); ++k)
         ptx::mma_ts(d_tmem, a_tmem + k * 8, dv + (uint64_t)((k * 16 * 128) >> 4), idesc_o,
                     (acc || k > 0) ? 1u : 0u);
 #endif
@@ -582,10 +593,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (j < nt) {
             const uint32_t ph = (t == 0) ? p_phase0 : p_phase1;
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < kPParts; ++h) {
               if (t == 0) { ATTN_TIMED(w_p0, ptx::mbar_wait(&ctrl->p_ready[t][h], ph)); }
               else { ATTN_TIMED(w_p1, ptx::mbar_wait(&ctrl->p_ready[t][h], ph)); }
-              if (h == 1) { ATTN_STAMP(2 + 2 * t); }
+              if (h == kPParts - 1) { ATTN_STAMP(2 + 2 * t); }
               ptx::tc_fence_after();
               if (ptx::elect_one_sync()) issue_pv_half(t, sV, j > 0, h);
               __syncwarp();
@@ -688,7 +699,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
 #ifdef ATTN_DEBUG_SKIP_SOFTMAX
         __syncwarp();
-        if (lane == 0) { ptx::mbar_arrive(&ctrl->p_ready[t][0]); ptx::mbar_arrive(&ctrl->p_ready[t][1]); }
+        if (lane == 0)
+          for (int h = 0; h < kPParts; ++h) ptx::mbar_arrive(&ctrl->p_ready[t][h]);
         l = 1.f;
         continue;
 #endif
@@ -710,6 +722,80 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = 0; k < kCols; ++k)
             if (k > lim) r[k] = 0xff800000u;
         }
+#if ATTN_SPEC_MAX
+        // Speculative block (j > 0, no masked keys): the threshold rule keeps
+        // m_use = m for every row whose block max stays within kRescaleThreshold
+        // of m, so half 0 of P is exponentiated against m while the block max
+        // is formed; if any row of the warp moves the max beyond the threshold,
+        // S is reloaded from TMEM (nothing has been written over it yet) and
+        // the block takes the general path below.  Bit-identical to it.
+        if constexpr (kSplit == 1 && kPParts == 2) {
+          if (j > 0 && !diag) {
+            const float negm = -m * c;
+            float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+            float2 sq[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                            make_float2(0.f, 0.f)};
+            auto exp_pair = [&](int k) {
+              const float2 x = ptx::ffma2(make_float2(__uint_as_float(r[k]), __uint_as_float(r[k + 1])), c, negm);
+              float2 pr;
+              constexpr int kEP = emu_period<D>();
+              if (kEP > 0 && ((k >> 1) % (kEP > 0 ? kEP : 1)) == kEP - 1) {
+                pr = ptx::ex2_poly2(x);
+              } else {
+                pr.x = ptx::ex2(x.x);
+                pr.y = ptx::ex2(x.y);
+              }
+              sq[(k >> 1) & 3] = ptx::fadd2(sq[(k >> 1) & 3], pr);
+              r[k >> 1] = ptx::pack_bf16(pr.x, pr.y);
+            };
+#pragma unroll
+            for (int k = 0; k < 64; k += 8) {
+#pragma unroll
+              for (int g4 = 0; g4 < 4; ++g4) {
+                mq[g4] = fmaxf(mq[g4], fmaxf(__uint_as_float(r[k + 2 * g4]), __uint_as_float(r[k + 2 * g4 + 1])));
+                exp_pair(k + 2 * g4);
+              }
+            }
+#pragma unroll
+            for (int k = 64; k < 128; k += 8) {
+#pragma unroll
+              for (int g4 = 0; g4 < 4; ++g4)
+                mq[g4] = fmaxf(mq[g4], fmaxf(__uint_as_float(r[k + 2 * g4]), __uint_as_float(r[k + 2 * g4 + 1])));
+            }
+            const float mxs = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
+#ifdef ATTN_TIMELINE
+            if (tl2) tl2[2] = clock64() + (long long)(mxs == 12345.f);
+#endif
+            if (!__any_sync(0xffffffffu, (mxs - m) * c > kRescaleThreshold)) {
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                if (h == 1) {
+#pragma unroll
+                  for (int k = 64; k < 128; k += 2) exp_pair(k);
+                }
+#ifdef ATTN_TIMELINE
+                if (tl2) tl2[6 + h] = clock64() + (long long)(r[h * 32] == 12345u);
+#endif
+                ptx::tmem_st32(trow + colP + h * 32, r + h * 32);
+                ptx::tmem_wait_st();
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&ctrl->p_ready[t][h]);
+#ifdef ATTN_TIMELINE
+                if (tls) tls[1 + h] = clock64();
+                if (tl2) tl2[3 + h] = clock64();
+#endif
+              }
+              const float2 s01 = ptx::fadd2(sq[0], sq[1]), s23 = ptx::fadd2(sq[2], sq[3]);
+              const float2 s4 = ptx::fadd2(s01, s23);
+              l = fmaf(l, 1.f, s4.x + s4.y);
+              continue;
+            }
+            // the max moved: reload S (intact in TMEM) and take the general path
+            ptx::tmem_ld128(trow + colS, r);
+          }
+        }
+#endif
         // row max: four independent FMNMX3 chains, then across the kSplit warps
         float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
@@ -761,9 +847,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                         make_float2(0.f, 0.f)};
         auto exp_block = [&](auto mask_tag) {
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < kPParts; ++h) {
 #pragma unroll
-          for (int k = h * kCols / 2; k < (h + 1) * kCols / 2; k += 2) {
+          for (int k = h * kCols / kPParts; k < (h + 1) * kCols / kPParts; k += 2) {
             const float2 x = ptx::ffma2(make_float2(__uint_as_float(r[k]), __uint_as_float(r[k + 1])), c, neg);
             float2 pr;
             constexpr int kEP = emu_period<D>();
@@ -784,15 +870,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             sq[(k >> 1) & 3] = ptx::fadd2(sq[(k >> 1) & 3], pr);
             r[k >> 1] = ptx::pack_bf16(pr.x, pr.y);
           }
-          if constexpr (kCols == 128) ptx::tmem_st32(trow + colP + h * 32, r + h * 32);
+          constexpr int kPc = kCols / kPParts / 2;  // packed P columns per slice
+#ifdef ATTN_TIMELINE
+          if (tl2 && (h == 0 || h == kPParts - 1)) tl2[6 + (h > 0)] = clock64() + (long long)(r[h * kPc] == 12345u);
+#endif
+          if constexpr (kPc == 32) ptx::tmem_st32(trow + colP + h * 32, r + h * 32);
           else ptx::tmem_st16(trow + colP + h * 16, r + h * 16);
           ptx::tmem_wait_st();
           ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&ctrl->p_ready[t][h]);
 #ifdef ATTN_TIMELINE
-          if (tls) tls[1 + h] = clock64();
-          if (tl2) tl2[3 + h] = clock64();
+          if (h == 0 || h == kPParts - 1) {
+            if (tls) tls[1 + (h > 0)] = clock64();
+            if (tl2) tl2[3 + (h > 0)] = clock64();
+          }
 #endif
         }
         };

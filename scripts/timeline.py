@@ -31,7 +31,9 @@ print("t0 issue done -> softmax0 next s_wake (median):", int(np.median(sm0[9:61,
 print("softmax0 p_h1 -> MMA p0_ok (median):", int(np.median(mma[9:61, 2] - sm0[9:61, 2])))
 # fine softmax stamps (tile 0 and 1): s_wake, ld done, max done, P half 0, P half 1, sum done
 for tt in (0, 1):
-    f = t[4096 + tt * 512: 4096 + tt * 512 + 64 * 8].reshape(64, 8)[:, :6] - t0
-    dd = np.median(np.diff(f[8:60], axis=1), axis=0).astype(int)
-    print(f"tile {tt} softmax phases (median cycles): ld {dd[0]}  max {dd[1]}  exp+st half0 {dd[2]}  "
-          f"exp+st half1 {dd[3]}  sum {dd[4]}  total {int(np.median(f[8:60, 5] - f[8:60, 0]))}")
+    f = t[4096 + tt * 512: 4096 + tt * 512 + 64 * 8].reshape(64, 8) - t0
+    # stamps: 0 s_wake, 1 ld done, 2 max done, 6 exps h0 done, 3 P h0 published, 7 exps h1 done, 4 P h1 published, 5 sum
+    g = f[8:60][:, [0, 1, 2, 6, 3, 7, 4, 5]]
+    dd = np.median(np.diff(g, axis=1), axis=0).astype(int)
+    print(f"tile {tt} softmax phases (median cycles): ld {dd[0]}  max {dd[1]}  exps h0 {dd[2]}  st+publish h0 {dd[3]}  "
+          f"exps h1 {dd[4]}  st+publish h1 {dd[5]}  sum {dd[6]}  total {int(np.median(f[8:60, 5] - f[8:60, 0]))}")
