@@ -237,6 +237,17 @@ def run_ours(a):
             if prof:
                 by_mapping[m]["dram_gb_per_launch"] = round(prof["dram_bytes_per_launch"] / 1e9, 3)
 
+    # replicated output (N > 1, forward): the kernel epilogue storing O into
+    # every rank's buffer over NVLink (attn_fwd_replicated + CUDA IPC) vs the
+    # forward followed by an NCCL all-gather of O; device-timed, max over ranks
+    replicated = None
+    if world > 1 and a.pass_ == "fwd" and not a.no_replicated:
+        try:
+            replicated = measure_replicated(api, pdist, sets[0], shard, (B, Hq_job, N, d), causal, scale, a.mapping,
+                                            rank, world, dev, stream)
+        except Exception as e:  # reported, never fatal to the main line
+            replicated = {"error": repr(e)[:300]}
+
     # end to end through the public API on pinned host buffers
     e2e_steps = max(2, min(a.steps, 10))
     if a.pass_ == "fwd":
@@ -309,6 +320,8 @@ def run_ours(a):
         "gpu_launches": launches,
         "clocks": clocks,
     }
+    if replicated is not None:
+        out["replicated_output"] = replicated
     if rank == 0 and world == 1 and not a.no_cpu_baseline and a.pass_ == "fwd":
         out["cpu_baseline"] = cpu_baseline(a.workload, a.cpu_seconds)
     if rank == 0:
@@ -316,6 +329,54 @@ def run_ours(a):
     if world > 1:
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()
+
+
+def measure_replicated(api, pdist, qkvo, shard, full_shape, causal, scale, mapping, rank, world, dev, stream,
+                       reps=5):
+    import torch
+    import torch.distributed as tdist
+
+    q, k, v, o = qkvo
+    po = pdist.PeerOutput(full_shape, rank, world, dev)
+    dsts = [po.ptrs[rank]] + [p for r, p in enumerate(po.ptrs) if r != rank]
+    nccl = tdist.get_backend() == "nccl"
+    gbuf = torch.empty((world,) + tuple(o.shape), dtype=o.dtype, device=dev) if nccl else None
+
+    def fused():
+        api.attn_fwd_replicated(q, k, v, dsts, full_shape[1], shard.q_lo, causal=causal, scale=scale,
+                                mapping=mapping, stream=stream)
+
+    def gathered():
+        api.attn_fwd(q, k, v, o, causal=causal, scale=scale, mapping=mapping, stream=stream)
+        tdist.all_gather_into_tensor(gbuf, o)
+
+    def time_it(fn):
+        ts = []
+        for i in range(reps + 2):
+            torch.cuda.synchronize()
+            tdist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            if i >= 2:
+                ts.append(e0.elapsed_time(e1))
+        ts.sort()
+        return pdist.max_over_ranks(ts[len(ts) // 2], dev)
+
+    res = {"fused_peer_store_ms": round(time_it(fused), 4),
+           "fwd_then_nccl_allgather_ms": round(time_it(gathered), 4) if nccl else None,
+           "o_bytes_per_rank": o.numel() * o.element_size(),
+           "method": "attn_fwd_replicated: epilogue stores each O tile into all ranks' buffers (CUDA IPC, NVLink "
+                     "P2P); vs attn_fwd + all_gather_into_tensor; median of 5, device events, max over ranks"}
+    # the fused result must equal the gathered one (heads are independent)
+    tdist.barrier()
+    if nccl:
+        ref = gbuf.permute(1, 0, 2, 3, 4).reshape(full_shape)
+        res["bit_identical"] = bool(torch.equal(po.local.view(torch.int16), ref.view(torch.int16)))
+    po.close()
+    return res
 
 
 class _Null:
@@ -428,6 +489,8 @@ def main():
     ap.add_argument("--mapping", default="swizzled_head_first", choices=MAPS)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-replicated", action="store_true",
+                    help="N > 1: skip the replicated-output (fused peer-store vs NCCL all-gather) measurement")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--sets", type=int, default=0, help="resident input sets rotated per step (0: auto)")
     ap.add_argument("--flush", action="store_true", help="memset a 2xL2 buffer before every step")

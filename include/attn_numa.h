@@ -175,6 +175,45 @@ ATTN_API int attn_bwd(const void* q, const void* k, const void* v, const void* o
 ATTN_API int attn_fwd_host(const void* q_host, const void* k_host, const void* v_host, void* o_host, int B, int Hq,
                   int Hkv, int N, int d, int causal, float scale, int mapping, void* cuda_stream);
 
+/* Head-sharded forward with REPLICATED output stored by the kernel itself
+ * (the fused alternative to an all-gather of O; heads are
+ * independent).  q, k, v are this rank's shard ([B][Hq][N][d],
+ * [B][Hkv][N][d], device memory of the current device; B, Hq, Hkv are the
+ * SHARD's sizes).  o_dst is a HOST array of n_dst (1..ATTN_MAX_DST) device
+ * pointers, each a full output [B][Hq_out][N][d] bf16: this device's own
+ * buffer, or a peer GPU's buffer mapped into this process (attn_ipc_open;
+ * NVLink P2P).  The epilogue stores every finished O tile of head h into
+ * every o_dst[i] at head head_offset + h, so after all ranks' kernels have
+ * completed (the caller synchronises its stream and then the ranks, e.g. a
+ * process-group barrier) each rank holds the whole [B][Hq_out][N][d] result.
+ * Only the shard's heads are written; the values are bit-identical to
+ * attn_fwd on the shard.  Needs 0 <= head_offset, head_offset + Hq <= Hq_out;
+ * destinations must not overlap each other or the inputs.  Same status
+ * codes as attn_fwd (ATTN_CLUSTER_MULTICAST and ATTN_ORDER_DESCENDING apply). */
+#define ATTN_MAX_DST 8
+ATTN_API int attn_fwd_replicated(const void* q, const void* k, const void* v, void* const* o_dst, int n_dst,
+                                 int Hq_out, int head_offset, int B, int Hq, int Hkv, int N, int d, int causal,
+                                 float scale, int mapping, void* cuda_stream);
+
+/* CUDA IPC for attn_fwd_replicated's peer destinations.  attn_ipc_get_handle
+ * exports the allocation containing dev_ptr (device memory of the current
+ * device, from cudaMalloc, e.g. torch's caching allocator) and records
+ * dev_ptr's offset in it; the 72-byte record is sent to the other ranks (any
+ * byte transport).  attn_ipc_open, in ANOTHER process, maps it on the current
+ * device (peer access enabled lazily) and returns the address of dev_ptr in
+ * that mapping; attn_ipc_close unmaps a pointer attn_ipc_open returned.  The
+ * exporting process must keep the allocation alive until every importer has
+ * closed it.  Errors: ATTN_ERR_INVALID_VALUE (null / foreign pointer),
+ * ATTN_ERR_CUDA (the CUDA IPC call failed, e.g. opening a handle in the
+ * process that exported it). */
+typedef struct {
+  unsigned char handle[64]; /* cudaIpcMemHandle_t of the containing allocation */
+  long long offset;         /* dev_ptr - allocation base */
+} attn_ipc_handle_t;
+ATTN_API int attn_ipc_get_handle(const void* dev_ptr, attn_ipc_handle_t* out);
+ATTN_API int attn_ipc_open(const attn_ipc_handle_t* h, void** dev_ptr_out);
+ATTN_API int attn_ipc_close(void* dev_ptr);
+
 /* Thread-local default stream for attn_fwd. */
 ATTN_API int attn_set_stream(void* cuda_stream);
 

@@ -19,6 +19,7 @@ EXPORTS = (
     "attn_fwd", "attn_fwd_stream", "attn_fwd_lse", "attn_bwd", "attn_fwd_host", "attn_set_stream", "attn_init", "attn_topology",
     "attn_set_topology_override", "attn_set_schedule_trace", "attn_schedule_order",
     "attn_last_launch_info", "attn_status_string", "attn_last_error", "attn_version", "attn_shutdown",
+    "attn_fwd_replicated", "attn_ipc_get_handle", "attn_ipc_open", "attn_ipc_close",
 )
 
 
@@ -51,6 +52,10 @@ class LaunchInfo(ctypes.Structure):
                 ("units", ctypes.c_int), ("n_queues", ctypes.c_int), ("kernel_launches", ctypes.c_int)]
 
 
+class IpcHandle(ctypes.Structure):
+    _fields_ = [("handle", ctypes.c_ubyte * 64), ("offset", ctypes.c_longlong)]
+
+
 _lib = None
 
 
@@ -78,9 +83,14 @@ def load():
     lib.attn_set_schedule_trace.argtypes = [i32, vp, ll]
     lib.attn_schedule_order.argtypes = [i32, i32, i32, i32, i32, i32, vp, vp, ll, vp, vp]
     lib.attn_last_launch_info.argtypes = [ctypes.POINTER(LaunchInfo)]
+    lib.attn_fwd_replicated.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, i32, i32, f32, i32, vp]
+    lib.attn_ipc_get_handle.argtypes = [vp, ctypes.POINTER(IpcHandle)]
+    lib.attn_ipc_open.argtypes = [ctypes.POINTER(IpcHandle), ctypes.POINTER(ctypes.c_void_p)]
+    lib.attn_ipc_close.argtypes = [vp]
     for f in ("attn_fwd", "attn_fwd_stream", "attn_fwd_lse", "attn_bwd", "attn_fwd_host", "attn_set_stream", "attn_init", "attn_topology",
               "attn_set_topology_override", "attn_set_schedule_trace", "attn_schedule_order",
-              "attn_last_launch_info"):
+              "attn_last_launch_info", "attn_fwd_replicated", "attn_ipc_get_handle", "attn_ipc_open",
+              "attn_ipc_close"):
         getattr(lib, f).restype = i32
     lib.attn_status_string.argtypes = [i32]
     lib.attn_status_string.restype = ctypes.c_char_p

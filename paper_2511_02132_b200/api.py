@@ -88,6 +88,54 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: Optional[torc
     return o
 
 
+def attn_fwd_replicated(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o_dst: Sequence, Hq_out: int,
+                        head_offset: int, *, causal: bool = False, scale: Optional[float] = None,
+                        mapping="swizzled_head_first", order: str = "ascending",
+                        stream: Optional[torch.cuda.Stream] = None, cluster: bool = False) -> None:
+    """Head-shard forward whose epilogue stores O into every destination (C-ABI attn_fwd_replicated).
+
+    q/k/v: this rank's shard; o_dst: full [B, Hq_out, N, d] outputs, given as
+    bf16 CUDA tensors (this device) or raw device addresses (peer buffers
+    mapped with ipc_open).  The shard's heads land at head_offset."""
+    B, Hq, N, d = q.shape
+    if not 1 <= len(o_dst) <= 8:
+        raise ValueError("1 to 8 destinations")
+    ptrs = []
+    for t in o_dst:
+        if isinstance(t, torch.Tensor):
+            if t.dtype != torch.bfloat16 or not t.is_contiguous() or tuple(t.shape) != (B, Hq_out, N, d):
+                raise ValueError("each destination must be a contiguous bf16 [B, Hq_out, N, d] tensor")
+            ptrs.append(t.data_ptr())
+        else:
+            ptrs.append(int(t))
+    if scale is None:
+        scale = 1.0 / math.sqrt(d)
+    arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
+    lib = _lib.load()
+    _check(lib.attn_fwd_replicated(q.data_ptr(), k.data_ptr(), v.data_ptr(), arr, len(ptrs), int(Hq_out),
+                                   int(head_offset), B, Hq, k.shape[1], N, d, int(bool(causal)), float(scale),
+                                   _mapping_id(mapping, order, cluster), _stream_ptr(stream)))
+
+
+def ipc_get_handle(t: torch.Tensor) -> bytes:
+    """72-byte CUDA IPC record (handle + offset) for a CUDA tensor's storage (C-ABI attn_ipc_get_handle)."""
+    h = _lib.IpcHandle()
+    _check(_lib.load().attn_ipc_get_handle(t.data_ptr(), ctypes.byref(h)))
+    return bytes(h)
+
+
+def ipc_open(record: bytes) -> int:
+    """Map another process's ipc_get_handle record on the current device; returns the device address."""
+    h = _lib.IpcHandle.from_buffer_copy(record)
+    p = ctypes.c_void_p()
+    _check(_lib.load().attn_ipc_open(ctypes.byref(h), ctypes.byref(p)))
+    return int(p.value)
+
+
+def ipc_close(ptr: int) -> None:
+    _check(_lib.load().attn_ipc_close(ctypes.c_void_p(ptr)))
+
+
 def attn_fwd_lse(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool = False,
                  scale: Optional[float] = None, mapping="swizzled_head_first", order: str = "ascending",
                  stream: Optional[torch.cuda.Stream] = None, cluster: bool = False):

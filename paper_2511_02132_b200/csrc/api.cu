@@ -432,15 +432,67 @@ int launch_t(DevState& st, int attr_idx, const CUtensorMap& tq, const CUtensorMa
   return ATTN_OK;
 }
 
+// Where the epilogue stores O (attn_fwd_replicated): n destinations of
+// [B][Hq_out][N][d], the shard's heads at h_off.
+struct OutSpec {
+  void* const* dst;
+  int n, Hq_out, h_off;
+};
+
+// A destination must be device memory of this device or of a peer this
+// device can access (NVLink P2P, e.g. an attn_ipc_open mapping).
+int check_dst_ptr(const void* p, int dev, int i) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(ATTN_ERR_INVALID_VALUE, "o_dst[" + std::to_string(i) + "] is not a CUDA pointer");
+  }
+  if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged)
+    return fail(ATTN_ERR_INVALID_VALUE, "o_dst[" + std::to_string(i) + "] is not device memory");
+  if (a.type == cudaMemoryTypeDevice && a.device != dev) {
+    int can = 0;
+    if (cudaDeviceCanAccessPeer(&can, dev, a.device) != cudaSuccess || !can) {
+      cudaGetLastError();
+      return fail(ATTN_ERR_INVALID_VALUE, "o_dst[" + std::to_string(i) + "] is on a device without peer access");
+    }
+  }
+  return ATTN_OK;
+}
+
+int validate_out(const OutSpec& out, const void* q, const void* k, const void* v, int B, int Hq, int Hkv, int N,
+                 int d, int dev) {
+  if (!out.dst || out.n < 1 || out.n > kMaxDst)
+    return fail(ATTN_ERR_INVALID_VALUE, "n_dst must be in [1, ATTN_MAX_DST]");
+  if (out.Hq_out < Hq || out.h_off < 0 || out.h_off > out.Hq_out - Hq)
+    return fail(ATTN_ERR_INVALID_VALUE, "need 0 <= head_offset and head_offset + Hq <= Hq_out");
+  if ((long long)B * out.Hq_out * N >= (1ll << 31)) return fail(ATTN_ERR_UNSUPPORTED, "B*Hq_out*N exceeds 2^31 rows");
+  const size_t ob = (size_t)B * out.Hq_out * N * d * 2;
+  const size_t qb = (size_t)B * Hq * N * d * 2, kb = (size_t)B * Hkv * N * d * 2;
+  for (int i = 0; i < out.n; ++i) {
+    const void* o = out.dst[i];
+    if (!o) return fail(ATTN_ERR_INVALID_VALUE, "null o_dst[" + std::to_string(i) + "]");
+    if (reinterpret_cast<uintptr_t>(o) % 16 != 0) return fail(ATTN_ERR_UNSUPPORTED, "o_dst pointer not 16-byte aligned");
+    if (overlaps(o, ob, q, qb) || overlaps(o, ob, k, kb) || overlaps(o, ob, v, kb))
+      return fail(ATTN_ERR_INVALID_VALUE, "o_dst[" + std::to_string(i) + "] overlaps an input");
+    for (int j = 0; j < i; ++j)
+      if (overlaps(o, ob, out.dst[j], ob)) return fail(ATTN_ERR_INVALID_VALUE, "o_dst buffers overlap");
+    int rc = check_dst_ptr(o, dev, i);
+    if (rc != ATTN_OK) return rc;
+  }
+  return ATTN_OK;
+}
+
 int fwd_impl(const void* q, const void* k, const void* v, void* o, int B, int Hq, int Hkv, int N, int d, int causal,
-             float scale, int mapping, cudaStream_t stream, float* lse = nullptr) {
+             float scale, int mapping, cudaStream_t stream, float* lse = nullptr, const OutSpec* out = nullptr) {
   int rc = validate(q, k, v, o, B, Hq, Hkv, N, d, scale, mapping);
   if (rc != ATTN_OK) return rc;
   int dev = 0;
   rc = current_device(dev);
   if (rc != ATTN_OK) return rc;
+  if (out && (rc = validate_out(*out, q, k, v, B, Hq, Hkv, N, d, dev)) != ATTN_OK) return rc;
   for (auto pr : {std::make_pair(q, "q"), std::make_pair(k, "k"), std::make_pair(v, "v"),
                   std::make_pair((const void*)o, "o")}) {
+    if (out && pr.first == o) continue;  // replicated output: checked by validate_out (may be a peer buffer)
     rc = check_dev_ptr(pr.first, dev, pr.second);
     if (rc != ATTN_OK) return rc;
   }
@@ -470,6 +522,17 @@ int fwd_impl(const void* q, const void* k, const void* v, void* o, int B, int Hq
   const int dpad = d <= 64 ? 64 : 128;  // kernel head dim; TMA zero-fills columns d..dpad-1
   kp.scale_log2 = scale * 1.4426950408889634f;
   kp.o = reinterpret_cast<__nv_bfloat16*>(o);
+  if (out) {
+    for (int i = 0; i < out->n; ++i) kp.o_dst[i] = reinterpret_cast<__nv_bfloat16*>(out->dst[i]);
+    kp.n_dst = out->n;
+    kp.Hq_out = out->Hq_out;
+    kp.h_off = out->h_off;
+  } else {
+    kp.o_dst[0] = kp.o;
+    kp.n_dst = 1;
+    kp.Hq_out = Hq;
+    kp.h_off = 0;
+  }
   kp.lse = lse;
   if (!build_sched(mapping, B, Hsched, Hkv, Usched, st.active.n_domains, st.active.sms_per_domain, kp.sched))
     return fail(ATTN_ERR_INVALID_VALUE, "cannot build the schedule");
@@ -623,6 +686,67 @@ int attn_fwd_lse(const void* q, const void* k, const void* v, void* o, float* ls
     return fail(ATTN_ERR_INVALID_VALUE, "lse overlaps o or is misaligned");
   return fwd_impl(q, k, v, o, B, Hq, Hkv, N, d, causal, scale, mapping, reinterpret_cast<cudaStream_t>(cuda_stream),
                   lse);
+}
+
+int attn_fwd_replicated(const void* q, const void* k, const void* v, void* const* o_dst, int n_dst, int Hq_out,
+                        int head_offset, int B, int Hq, int Hkv, int N, int d, int causal, float scale, int mapping,
+                        void* cuda_stream) {
+  if (!o_dst || n_dst < 1 || n_dst > kMaxDst) return fail(ATTN_ERR_INVALID_VALUE, "n_dst must be in [1, ATTN_MAX_DST]");
+  const OutSpec out{o_dst, n_dst, Hq_out, head_offset};
+  return fwd_impl(q, k, v, o_dst[0], B, Hq, Hkv, N, d, causal, scale, mapping,
+                  reinterpret_cast<cudaStream_t>(cuda_stream), nullptr, &out);
+}
+
+int attn_ipc_get_handle(const void* dev_ptr, attn_ipc_handle_t* out) {
+  if (!dev_ptr || !out) return fail(ATTN_ERR_INVALID_VALUE, "null pointer");
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult qr;
+  if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &qr) != cudaSuccess || !fn)
+    return fail(ATTN_ERR_CUDA, "cuMemGetAddressRange unavailable");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(fn)(&base, &size, (CUdeviceptr)dev_ptr) != CUDA_SUCCESS)
+    return fail(ATTN_ERR_INVALID_VALUE, "dev_ptr is not inside a device allocation");
+  cudaIpcMemHandle_t h;
+  ATTN_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+  static_assert(sizeof(h) == sizeof(out->handle), "cudaIpcMemHandle_t size");
+  std::memcpy(out->handle, &h, sizeof(h));
+  out->offset = (long long)((CUdeviceptr)dev_ptr - base);
+  return ATTN_OK;
+}
+
+namespace {
+std::mutex g_ipc_mu;
+std::vector<std::pair<void*, void*>> g_ipc_open;  // (returned pointer, mapped base)
+}  // namespace
+
+int attn_ipc_open(const attn_ipc_handle_t* h, void** dev_ptr_out) {
+  if (!h || !dev_ptr_out || h->offset < 0) return fail(ATTN_ERR_INVALID_VALUE, "bad handle or null output");
+  cudaIpcMemHandle_t ch;
+  std::memcpy(&ch, h->handle, sizeof(ch));
+  void* base = nullptr;
+  ATTN_CUDA(cudaIpcOpenMemHandle(&base, ch, cudaIpcMemLazyEnablePeerAccess));
+  void* p = static_cast<char*>(base) + h->offset;
+  std::lock_guard<std::mutex> lk(g_ipc_mu);
+  g_ipc_open.emplace_back(p, base);
+  *dev_ptr_out = p;
+  return ATTN_OK;
+}
+
+int attn_ipc_close(void* dev_ptr) {
+  void* base = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_ipc_mu);
+    for (size_t i = 0; i < g_ipc_open.size(); ++i)
+      if (g_ipc_open[i].first == dev_ptr) {
+        base = g_ipc_open[i].second;
+        g_ipc_open.erase(g_ipc_open.begin() + i);
+        break;
+      }
+  }
+  if (!base) return fail(ATTN_ERR_INVALID_VALUE, "pointer was not returned by attn_ipc_open");
+  ATTN_CUDA(cudaIpcCloseMemHandle(base));
+  return ATTN_OK;
 }
 
 int attn_bwd(const void* q, const void* k, const void* v, const void* o, const void* dout, const float* lse, void* dq,

@@ -115,6 +115,8 @@ struct Cfg {
   static __device__ __forceinline__ uint32_t col_o(int t) { return 256u + (uint32_t)D * t; }
 };
 
+constexpr int kMaxDst = 8;  // ATTN_MAX_DST
+
 struct KernelParams {
   int B, Hq, Hkv, N, G, U, nblk;
   int Usched;        // units per head in the queues: U, or ceil(U/2) cluster units (kCl == 2, adjacent mode)
@@ -123,7 +125,13 @@ struct KernelParams {
                      //           0 = the pair takes units 2u', 2u'+1 of one head
   int d_real;        // head dim of the tensors (<= D; TMA zero-fills columns d_real..D-1)
   float scale_log2;  // scale * log2(e), >= 0
-  __nv_bfloat16* o;
+  __nv_bfloat16* o;   // == o_dst[0]
+  // Output destinations (replicated output, SURVEY §8(e) fused alternative):
+  // every finished O tile is stored into each o_dst[i], a [B][Hq_out][N][d]
+  // buffer, at head h_off + h.  Plain call: n_dst = 1, Hq_out = Hq, h_off = 0.
+  // Peer destinations are NVLink-mapped buffers of other GPUs (P2P stores).
+  __nv_bfloat16* o_dst[kMaxDst];
+  int n_dst, Hq_out, h_off;
   float* lse;        // optional [B][Hq][N] natural-log row LSE (backward input), may be null
   SchedParams sched;
   int* counters;                 // one int per queue, 32 ints apart, then the done count
@@ -911,8 +919,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float inv_l = 1.f / l;
       if (p.lse != nullptr && hf == 0 && qb * kBlockM + row < p.N)  // lse = scale*m + ln(l)
         p.lse[(long long)(e.x * p.Hq + hh) * p.N + qb * kBlockM + row] = (m * c + __log2f(l)) * 0.6931471805599453f;
-      const long long orow = ((long long)(e.x * p.Hq + hh) * p.N + (long long)qb * kBlockM + row) * p.d_real;
-      uint4* dst = reinterpret_cast<uint4*>(p.o + orow + hf * kOCols);
+      const long long orow =
+          ((long long)(e.x * p.Hq_out + p.h_off + hh) * p.N + (long long)qb * kBlockM + row) * p.d_real + hf * kOCols;
       // real columns of this thread's slice (multiple of 8); rows >= N (ragged
       // last query block) store nothing but still join the warp-wide TMEM loads
       const int ncol = (qb * kBlockM + row < p.N) ? p.d_real - hf * kOCols : 0;
@@ -924,14 +932,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int k = 0; k < 16; ++k)
           pk[k] = ptx::pack_bf16(__uint_as_float(o[2 * k]) * inv_l, __uint_as_float(o[2 * k + 1]) * inv_l);
+        for (int di = 0; di < p.n_dst; ++di) {  // replicated output: one store per destination
+          uint4* dst = reinterpret_cast<uint4*>(p.o_dst[di] + orow);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          if (cc + 8 * k >= ncol) break;  // padded head dim: the zero columns are not stored
+          for (int k = 0; k < 4; ++k) {
+            if (cc + 8 * k >= ncol) break;  // padded head dim: the zero columns are not stored
 #if ATTN_O_EVICT_FIRST
-          ptx::st_global_v4_evict_first(dst + cc / 8 + k, make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]), pol_o);
+            ptx::st_global_v4_evict_first(dst + cc / 8 + k, make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]), pol_o);
 #else
-          dst[cc / 8 + k] = make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
+            dst[cc / 8 + k] = make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
 #endif
+          }
         }
       }
       ptx::tc_fence_before();

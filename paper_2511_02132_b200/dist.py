@@ -99,3 +99,55 @@ def max_over_ranks(x: float, device=None) -> float:
     t = torch.tensor([float(x)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+class PeerOutput:
+    """A full-size output [B, Hq, N, d] on every rank, mapped into every other
+    rank's address space (CUDA IPC; NVLink P2P between GPUs of one node), so
+    the forward's epilogue can store each finished O tile straight into all
+    ranks' copies (C-ABI attn_fwd_replicated) instead of an all-gather after
+    the kernel (fused alternative).
+
+    ptrs[r] is rank r's buffer as seen from this process (this rank's own
+    tensor for r == rank).  Collective: every rank of `group` must construct
+    it with the same shape.  close() unmaps the peers (also collective)."""
+
+    def __init__(self, shape, rank: int, world: int, device, group=None, api=None):
+        if api is None:
+            from . import api as api_mod
+            api = api_mod
+        self._api = api
+        self.rank, self.world, self.group = rank, world, group
+        self.local = torch.empty(tuple(shape), dtype=torch.bfloat16, device=device)
+        rec = api.ipc_get_handle(self.local) if world > 1 else b""
+        recs = [None] * world
+        if world > 1:
+            dist.all_gather_object(recs, rec, group=group)
+        self.ptrs = [self.local.data_ptr() if r == rank else api.ipc_open(recs[r]) for r in range(world)]
+
+    def close(self) -> None:
+        for r, p in enumerate(self.ptrs):
+            if r != self.rank:
+                self._api.ipc_close(p)
+        self.ptrs = [self.local.data_ptr() if r == self.rank else 0 for r in range(self.world)]
+        if self.world > 1:
+            dist.barrier(group=self.group)  # no rank frees its buffer while a peer still maps it
+
+
+def replicated_fwd(q, k, v, shard: HeadShard, out: PeerOutput, *, causal: bool = False, scale=None,
+                   mapping="swizzled_head_first", sync: bool = True, api=None, **kw) -> torch.Tensor:
+    """This rank's head shard forward, its O tiles stored into every rank's
+    PeerOutput buffer by the kernel epilogue (own buffer first).  With sync,
+    waits for the stream and then for all ranks, after which out.local holds
+    the whole output.  Shard heads land at shard.q_lo."""
+    if api is None:
+        from . import api as api_mod
+        api = api_mod
+    dsts = [out.ptrs[out.rank]] + [p for r, p in enumerate(out.ptrs) if r != out.rank]
+    Hq_out = out.local.shape[1]
+    api.attn_fwd_replicated(q, k, v, dsts, Hq_out, shard.q_lo, causal=causal, scale=scale, mapping=mapping, **kw)
+    if sync:
+        torch.cuda.current_stream().synchronize()
+        if out.world > 1:
+            dist.barrier(group=out.group)
+    return out.local

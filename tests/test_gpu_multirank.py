@@ -34,6 +34,8 @@ def test_bench_two_ranks_share_gpu(workload, scaling):
     assert len(lines) == 1, out.stdout[-2000:]
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["scaling"] == scaling and d["gpu_launches"] == int(steps)
+    rep = d["replicated_output"]  # fused peer-store epilogue over CUDA IPC (both ranks on cuda:0)
+    assert "error" not in rep and rep["fused_peer_store_ms"] > 0, rep
     if workload == "C2":
         assert d["config"]["Hq"] == 64 and d["config"]["heads_per_gpu"] == 32  # weak: 32 heads per rank
     else:
