@@ -59,6 +59,13 @@ constexpr int kPParts = ATTN_P_PARTS;
 #ifndef ATTN_SPEC_MAX
 #define ATTN_SPEC_MAX 0
 #endif
+// Head dim <= 64 (plain CTAs): P gets its own TMEM columns (the 128 that
+// S0 S1 O0 O1 leave free) instead of aliasing S, so S_t(j+1) is issued as soon
+// as the softmax has loaded S_t(j) into registers and each tile's softmax runs
+// back to back instead of waiting for the PV -> S -> softmax round trip.
+#ifndef ATTN_SEP_P
+#define ATTN_SEP_P 1
+#endif
 // softmax warps per (tile, TMEM lane quarter): each handles kBlockN / kSplit
 // columns of its 32 rows, so two warps share each SMSP's MUFU per tile.
 constexpr int kSplit = ATTN_SPLIT;
@@ -113,6 +120,8 @@ struct Cfg {
   // TMEM columns: S_t at 128*t, O_t at 256 + D*t
   static __device__ __forceinline__ uint32_t col_s(int t) { return 128u * t; }
   static __device__ __forceinline__ uint32_t col_o(int t) { return 256u + (uint32_t)D * t; }
+  // separate-P layout (D <= 64): P_t (bf16 pairs, 64 columns) after O1
+  static __device__ __forceinline__ uint32_t col_p(int t) { return 256u + 2u * D + 64u * t; }
 };
 
 constexpr int kMaxDst = 8;  // ATTN_MAX_DST
@@ -150,6 +159,8 @@ struct __align__(16) Ctrl {
   uint64_t s_ready[2];
   uint64_t p_ready[2][4];   // [tile][slice of P]  softmax -> MMA
   uint64_t o_ready[2];
+  uint64_t s_free[2];       // separate-P layout: softmax loaded S_t -> MMA may overwrite it
+  uint64_t p_free[2];       // separate-P layout: PV_t done reading P_t (and adding into O_t)
   int4 entry[kSchedRing];  // (b, h, u, valid)
   uint32_t tmem_base;
 };
@@ -322,6 +333,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   static_assert(C::kSmemBytes <= 232448, "shared memory exceeds 227 KB");
 
   static_assert(kCl == 1 || kCl == 2, "cluster size 1 or 2");
+  constexpr bool kSepP = ATTN_SEP_P && D <= 64 && kCl == 1;
+  static_assert(!kSepP || 256 + 2 * D + 128 <= kTmemCols, "separate P does not fit in TMEM");
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t crank = (kCl > 1) ? ptx::cluster_ctarank() : 0u;
@@ -344,6 +357,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int h = 0; h < kPParts; ++h)
         ptx::mbar_init(&ctrl->p_ready[i][h], 4 * kSplit);  // one arrive per softmax warp of the tile
       ptx::mbar_init(&ctrl->o_ready[i], 1);
+      ptx::mbar_init(&ctrl->s_free[i], 4 * kSplit);
+      ptx::mbar_init(&ctrl->p_free[i], 1);
     }
     ptx::fence_barrier_init();
   }
@@ -492,6 +507,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     [[maybe_unused]] int extra_blocks = 0;
     int kv_stage = 0;
     uint32_t kv_phase = 0;
+    [[maybe_unused]] int s_used0 = 0, s_used1 = 0;
+    [[maybe_unused]] uint32_t sf_phase0 = 0, sf_phase1 = 0;
 
     auto issue_s = [&](int t, int slot) {
       const uint64_t dq = dq0 + (uint64_t)((t * C::kQTileBytes) >> 4);
@@ -511,7 +528,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto issue_pv_half = [&](int t, int slot, bool acc, int h) {
       const uint64_t dv = dv0 + (uint64_t)((slot * C::kKVBytes) >> 4);
       const uint32_t d_tmem = tmem + C::col_o(t);
-      const uint32_t a_tmem = tmem + C::col_s(t);
+      const uint32_t a_tmem = tmem + (kSepP ? C::col_p(t) : C::col_s(t));
 #ifndef ATTN_DEBUG_NO_PV
 #pragma unroll
       for (int k = h * (8 / kPParts); k < (h + 1) * (8 / kPParts); ++k)
@@ -562,6 +579,71 @@ __global__ void __launch_bounds__(kThreads, 1)
           continue;
         }
         extra_blocks = n_all - n;
+      }
+      if constexpr (kSepP) {
+        // Separate-P order: S_t(j+1) as soon as the softmax has S_t(j) in
+        // registers (s_free), PV_t(j) when P_t(j) is published; p_free / o_ready
+        // tell the softmax when P_t may be overwritten and O_t rescaled / read.
+        ATTN_TIMED(w_q, ptx::mbar_wait(&ctrl->q_full, q_phase));
+        ++unit_no;
+        q_phase ^= 1;
+        auto issue_s_sep = [&](int t, int slot) {
+          int& used = (t == 0) ? s_used0 : s_used1;
+          uint32_t& sfp = (t == 0) ? sf_phase0 : sf_phase1;
+          if (used) {
+            ptx::mbar_wait(&ctrl->s_free[t], sfp);
+            sfp ^= 1;
+          }
+          used = 1;
+          ptx::tc_fence_after();
+          if (ptx::elect_one_sync()) {
+            issue_s(t, slot);
+            ptx::mma_commit(&ctrl->s_ready[t]);
+          }
+          __syncwarp();
+        };
+        int sK = take_slot();
+        if (n0 > 0) issue_s_sep(0, sK);
+        if (n1 > 0) issue_s_sep(1, sK);
+        if (ptx::elect_one_sync()) {
+          kv_release(sK);
+          if (n == 1) ptx::mma_commit(&ctrl->q_empty);
+        }
+        __syncwarp();
+        for (int j = 0; j < n; ++j) {
+          const int sV = take_slot();
+          if (j + 1 < n) {
+            sK = take_slot();
+            if (j + 1 < n0) issue_s_sep(0, sK);
+            if (j + 1 < n1) issue_s_sep(1, sK);
+            if (ptx::elect_one_sync()) {
+              kv_release(sK);
+              if (j + 2 == n) ptx::mma_commit(&ctrl->q_empty);
+            }
+            __syncwarp();
+          }
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            const int nt = (t == 0) ? n0 : n1;
+            if (j < nt) {
+              const uint32_t ph = (t == 0) ? p_phase0 : p_phase1;
+#pragma unroll
+              for (int h = 0; h < kPParts; ++h) {
+                if (t == 0) { ATTN_TIMED(w_p0, ptx::mbar_wait(&ctrl->p_ready[t][h], ph)); }
+                else { ATTN_TIMED(w_p1, ptx::mbar_wait(&ctrl->p_ready[t][h], ph)); }
+                ptx::tc_fence_after();
+                if (ptx::elect_one_sync()) issue_pv_half(t, sV, j > 0, h);
+                __syncwarp();
+              }
+              if (t == 0) p_phase0 ^= 1; else p_phase1 ^= 1;
+              if (ptx::elect_one_sync()) ptx::mma_commit(j + 1 < nt ? &ctrl->p_free[t] : &ctrl->o_ready[t]);
+              __syncwarp();
+            }
+          }
+          if (ptx::elect_one_sync()) kv_release(sV);
+          __syncwarp();
+        }
+        continue;
       }
       ATTN_TIMED(w_q, ptx::mbar_wait(&ctrl->q_full, q_phase));
       ++unit_no;
@@ -664,7 +746,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int cbase = hf * kCols;            // first key column of this thread's slice
     const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
     const uint32_t colS = C::col_s(t) + cbase;
-    const uint32_t colP = C::col_s(t) + cbase / 2;
+    const uint32_t colP = (kSepP ? C::col_p(t) : C::col_s(t)) + cbase / 2;
     const uint32_t colO = C::col_o(t) + hf * kOCols;
     [[maybe_unused]] const uint32_t bar_id = 1 + t * 4 + quarter;  // named barrier of the row group's warps
     const float c = p.scale_log2;
@@ -673,6 +755,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
     SchedReader<kCl> sr;
     uint32_t s_phase = 0, o_phase = 0, gblk = 0;
+    [[maybe_unused]] uint32_t pf_phase = 0;
     while (true) {
       const int4 e = sr.next(ctrl, false);
       __syncwarp();
@@ -707,6 +790,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
 #ifdef ATTN_DEBUG_SKIP_SOFTMAX
         __syncwarp();
+        if (kSepP && lane == 0) ptx::mbar_arrive(&ctrl->s_free[t]);
         if (lane == 0)
           for (int h = 0; h < kPParts; ++h) ptx::mbar_arrive(&ctrl->p_ready[t][h]);
         l = 1.f;
@@ -715,6 +799,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t r[kCols];
         if constexpr (kCols == 128) ptx::tmem_ld128(trow + colS, r);
         else ptx::tmem_ld64(trow + colS, r);
+        if constexpr (kSepP) {  // S_t is in registers: the MMA warp may compute S_t(j+1) over it
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&ctrl->s_free[t]);
+        }
 #ifdef ATTN_TIMELINE
         if (tl2) tl2[1] = clock64() + (r[0] & 0) + (r[kCols - 1] & 0);
 #endif
@@ -737,7 +826,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // is formed; if any row of the warp moves the max beyond the threshold,
         // S is reloaded from TMEM (nothing has been written over it yet) and
         // the block takes the general path below.  Bit-identical to it.
-        if constexpr (kSplit == 1 && kPParts == 2) {
+        if constexpr (kSplit == 1 && kPParts == 2 && !kSepP) {
           if (j > 0 && !diag) {
             const float negm = -m * c;
             float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
@@ -834,9 +923,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           m_use = m;
           alpha = 1.f;
         }
-        if (__any_sync(0xffffffffu, rescale)) {
-          // fix-up: O *= exp2((m_old - m_new) c) for this row;
-          // PV_t(j-1) is complete (it precedes S_t(j) in the MMA stream).
+        const bool any_rescale = __any_sync(0xffffffffu, rescale);
+        // fix-up: O *= exp2((m_old - m_new) c) for this row,
+        // once PV_t(j-1) is complete: it precedes S_t(j) in the MMA stream, or
+        // (separate-P layout) p_free says so, just before P_t(j) is stored.
+        auto fixup = [&]() {
 #pragma unroll
           for (int cc = 0; cc < kOCols; cc += 32) {
             uint32_t o[32];
@@ -845,7 +936,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int k = 0; k < 32; ++k) o[k] = __float_as_uint(__uint_as_float(o[k]) * alpha);
             ptx::tmem_st32(trow + colO + cc, o);
           }
-        }
+        };
+        if (!kSepP && any_rescale) fixup();
         const float neg = -m_use * c;
         // P = exp2(S c - m c) on (even, odd) pairs with packed f32x2 math:
         // MUFU.EX2 for most pairs, the FMA-pipe polynomial for every
@@ -877,6 +969,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             sq[(k >> 1) & 3] = ptx::fadd2(sq[(k >> 1) & 3], pr);
             r[k >> 1] = ptx::pack_bf16(pr.x, pr.y);
+          }
+          if constexpr (kSepP) {
+            if (h == 0 && j > 0) {  // PV_t(j-1) has finished reading P_t and adding into O_t
+              ptx::mbar_wait(&ctrl->p_free[t], pf_phase);
+              pf_phase ^= 1;
+              ptx::tc_fence_after();
+              if (any_rescale) fixup();
+            }
           }
           constexpr int kPc = kCols / kPParts / 2;  // packed P columns per slice
 #ifdef ATTN_TIMELINE
