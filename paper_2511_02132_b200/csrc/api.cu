@@ -17,7 +17,6 @@
 #include "../../include/attn_numa.h"
 #include "attn_bwd_sm100.cuh"
 #include "attn_fwd_sm100.cuh"
-#include "attn_fwd_n256_sm100.cuh"
 #include "attn_sched.h"
 #include "topology.cuh"
 
@@ -59,7 +58,7 @@ struct DevState {
   unsigned slot = 0;
   attn_trace_rec_t* trace = nullptr;
   long long trace_cap = 0;
-  bool attr_done[10] = {false, false, false, false, false, false, false, false, false, false};
+  bool attr_done[8] = {false, false, false, false, false, false, false, false};
   int max_clusters[4] = {0, 0, 0, 0};  // co-resident CTA-pair clusters per forward variant
   // e2e host-buffer path
   void* hbuf[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -433,37 +432,6 @@ int launch_t(DevState& st, int attr_idx, const CUtensorMap& tq, const CUtensorMa
   return ATTN_OK;
 }
 
-// Head dim 128 without clusters: the 256-key kernel (attn_fwd_n256_sm100.cuh)
-// unless ATTN_FWD_N256=0 in the environment (A/B measurements).
-#ifndef ATTN_FWD_N256_DEFAULT
-#define ATTN_FWD_N256_DEFAULT 0
-#endif
-bool use_n256() {
-  static const bool on = [] {
-    const char* e = std::getenv("ATTN_FWD_N256");
-    return e ? std::atoi(e) != 0 : ATTN_FWD_N256_DEFAULT != 0;
-  }();
-  return on;
-}
-
-template <bool kCausal>
-int launch_n256(DevState& st, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                const KernelParams& kp, int grid, cudaStream_t s) {
-  const int smem = n256::kSmemBytes;
-  auto* fn = n256::attn_fwd_n256_kernel<kCausal>;
-  const int idx = 8 + (kCausal ? 1 : 0);
-  if (!st.attr_done[idx]) {
-    ATTN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    st.attr_done[idx] = true;
-  }
-  fn<<<grid, kThreads, smem, s>>>(tq, tk, tv, kp);
-  ATTN_CUDA(cudaGetLastError());
-  g_info.grid = grid;
-  g_info.block = kThreads;
-  g_info.smem_bytes = smem;
-  return ATTN_OK;
-}
-
 // Where the epilogue stores O (attn_fwd_replicated): n destinations of
 // [B][Hq_out][N][d], the shard's heads at h_off.
 struct OutSpec {
@@ -585,9 +553,7 @@ int fwd_impl(const void* q, const void* k, const void* v, void* o, int B, int Hq
   const int total = B * Hq * U;
   const int cunits = B * Hsched * Usched;
   const int grid = std::min(st.num_sms, total);
-  if (dpad == 128 && !cluster && use_n256())
-    rc = causal ? launch_n256<true>(st, tq, tk, tv, kp, grid, stream) : launch_n256<false>(st, tq, tk, tv, kp, grid, stream);
-  else if (dpad == 128 && causal) rc = launch_t<128, true>(st, 0, tq, tk, tv, kp, grid, stream, cluster, cunits);
+  if (dpad == 128 && causal) rc = launch_t<128, true>(st, 0, tq, tk, tv, kp, grid, stream, cluster, cunits);
   else if (dpad == 128) rc = launch_t<128, false>(st, 1, tq, tk, tv, kp, grid, stream, cluster, cunits);
   else if (causal) rc = launch_t<64, true>(st, 2, tq, tk, tv, kp, grid, stream, cluster, cunits);
   else rc = launch_t<64, false>(st, 3, tq, tk, tv, kp, grid, stream, cluster, cunits);
