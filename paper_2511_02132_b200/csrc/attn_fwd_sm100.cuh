@@ -610,12 +610,22 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (n == 1) ptx::mma_commit(&ctrl->q_empty);
         }
         __syncwarp();
+#ifdef ATTN_TIMELINE
+        long long* tlm = (p.trace && blockIdx.x == 0 && unit_no == 0) ? reinterpret_cast<long long*>(p.trace) + 2048 : nullptr;
+#define ATTN_MSTAMP(i) if (tlm && lane == 0 && j < 64) tlm[j * 8 + (i)] = clock64();
+#else
+#define ATTN_MSTAMP(i)
+#endif
         for (int j = 0; j < n; ++j) {
+          ATTN_MSTAMP(0);
           const int sV = take_slot();
           if (j + 1 < n) {
             sK = take_slot();
+            ATTN_MSTAMP(1);
             if (j + 1 < n0) issue_s_sep(0, sK);
+            ATTN_MSTAMP(2);
             if (j + 1 < n1) issue_s_sep(1, sK);
+            ATTN_MSTAMP(3);
             if (ptx::elect_one_sync()) {
               kv_release(sK);
               if (j + 2 == n) ptx::mma_commit(&ctrl->q_empty);
@@ -631,6 +641,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int h = 0; h < kPParts; ++h) {
                 if (t == 0) { ATTN_TIMED(w_p0, ptx::mbar_wait(&ctrl->p_ready[t][h], ph)); }
                 else { ATTN_TIMED(w_p1, ptx::mbar_wait(&ctrl->p_ready[t][h], ph)); }
+                if (h == 1) { ATTN_MSTAMP(6 + t); }
                 ptx::tc_fence_after();
                 if (ptx::elect_one_sync()) issue_pv_half(t, sV, j > 0, h);
                 __syncwarp();
@@ -638,6 +649,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (t == 0) p_phase0 ^= 1; else p_phase1 ^= 1;
               if (ptx::elect_one_sync()) ptx::mma_commit(j + 1 < nt ? &ctrl->p_free[t] : &ctrl->o_ready[t]);
               __syncwarp();
+              ATTN_MSTAMP(4 + t);
             }
           }
           if (ptx::elect_one_sync()) kv_release(sV);
@@ -782,6 +794,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef ATTN_TIMELINE
         long long* tls = (p.trace && blockIdx.x == 0 && quarter == 0 && lane == 0 && first_unit && j < 64)
                              ? reinterpret_cast<long long*>(p.trace) + 600 + t * 200 + j * 3 : nullptr;
+        // every quarter's S wake-up and P h1 publication: [5120 + (t*4+quarter)*128 + 2j + {0,1}]
+        long long* tlq = (p.trace && blockIdx.x == 0 && lane == 0 && first_unit && j < 64)
+                             ? reinterpret_cast<long long*>(p.trace) + 5120 + (t * 4 + quarter) * 128 + 2 * j : nullptr;
+        if (tlq) tlq[0] = clock64();
         // fine stamps: [s_wake, ld done, max done, P half 0, P half 1, sum done]
         long long* tl2 = (p.trace && blockIdx.x == 0 && quarter == 0 && lane == 0 && first_unit && j < 64)
                              ? reinterpret_cast<long long*>(p.trace) + 4096 + t * 512 + j * 8 : nullptr;
@@ -991,6 +1007,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef ATTN_TIMELINE
           if (h == 0 || h == kPParts - 1) {
             if (tls) tls[1 + (h > 0)] = clock64();
+            if (tlq && h > 0) tlq[1] = clock64();
             if (tl2) tl2[3 + (h > 0)] = clock64();
           }
 #endif
