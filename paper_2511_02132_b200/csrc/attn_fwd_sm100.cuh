@@ -587,6 +587,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         ATTN_TIMED(w_q, ptx::mbar_wait(&ctrl->q_full, q_phase));
         ++unit_no;
         q_phase ^= 1;
+#ifdef ATTN_TIMELINE
+        long long* tlm = (p.trace && blockIdx.x == 0 && unit_no == 0) ? reinterpret_cast<long long*>(p.trace) + 2048 : nullptr;
+        int jst = -1;  // block index for the stamps inside issue_s_sep
+#endif
         auto issue_s_sep = [&](int t, int slot) {
           int& used = (t == 0) ? s_used0 : s_used1;
           uint32_t& sfp = (t == 0) ? sf_phase0 : sf_phase1;
@@ -594,6 +598,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_wait(&ctrl->s_free[t], sfp);
             sfp ^= 1;
           }
+#ifdef ATTN_TIMELINE
+          if (tlm && lane == 0 && jst >= 0 && jst < 64) tlm[512 + jst * 2 + t] = clock64();
+#endif
           used = 1;
           ptx::tc_fence_after();
           if (ptx::elect_one_sync()) {
@@ -611,8 +618,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
 #ifdef ATTN_TIMELINE
-        long long* tlm = (p.trace && blockIdx.x == 0 && unit_no == 0) ? reinterpret_cast<long long*>(p.trace) + 2048 : nullptr;
-#define ATTN_MSTAMP(i) if (tlm && lane == 0 && j < 64) tlm[j * 8 + (i)] = clock64();
+#define ATTN_MSTAMP(i) if (tlm && lane == 0 && j < 64) tlm[j * 8 + (i)] = clock64(); jst = j;
 #else
 #define ATTN_MSTAMP(i)
 #endif

@@ -42,3 +42,7 @@ for tt in (0, 1):
     pub = np.median(qq[tt, :, 8:40, 1] - qq[tt, 0:1, 8:40, 1], axis=1).astype(int)
     dur = np.median(qq[tt, :, 8:40, 1] - qq[tt, :, 8:40, 0], axis=1).astype(int)
     print(f"tile {tt} per quarter (vs quarter 0): s_wake {list(w)}  p_h1 {list(pub)}  s_wake->p_h1 {list(dur)}")
+sf = t[2048 + 512: 2048 + 512 + 128].reshape(64, 2)
+print(" j | s_free ok (tile 0, tile 1) relative to tile 0 s_wake of block j")
+for j in range(8, 16):
+    print(f"{j:2d} | " + " ".join(f"{x - sm[0][j, 0]:7d}" for x in sf[j]))
