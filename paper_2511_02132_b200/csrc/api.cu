@@ -26,7 +26,13 @@ using namespace attn;
 
 constexpr int kMaxDevices = 16;
 constexpr int kCounterSlots = 64;
-constexpr int kE2EChunks = 8;  // max chunks of the pipelined host-buffer path
+#ifndef ATTN_E2E_CHUNKS
+#define ATTN_E2E_CHUNKS 32
+#endif
+#ifndef ATTN_E2E_CHUNK_MB
+#define ATTN_E2E_CHUNK_MB 48
+#endif
+constexpr int kE2EChunks = ATTN_E2E_CHUNKS;  // max chunks of the pipelined host-buffer path
 constexpr int kCounterInts = (kMaxQueues + 1) * 32;  // one 128-byte line per queue + done count
 
 thread_local std::string g_err;
@@ -792,7 +798,7 @@ int attn_fwd_host(const void* q_host, const void* k_host, const void* v_host, vo
   // heads are independent, so the result is bit-identical to one call).
   // Three-stage pipeline: H2D chunk i+1 || kernel chunk i || D2H chunk i-1.
   const size_t total = 2 * nq + 2 * nk;
-  int target = (int)std::min<size_t>(kE2EChunks, std::max<size_t>(1, total / (48u << 20)));
+  int target = (int)std::min<size_t>(kE2EChunks, std::max<size_t>(1, total / ((size_t)ATTN_E2E_CHUNK_MB << 20)));
   const int tg = B * Hkv;
   target = std::min(target, tg);
   int gpc = (tg + target - 1) / target;  // KV groups per chunk
