@@ -436,9 +436,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         }
         const int kvbh = b * p.Hkv + h / p.G;
-        for (int j = 0; j < n; ++j) {
+        for (int jj = 0; jj < n; ++jj) {
 #pragma unroll
-          for (int which = 0; which < 2; ++which) {
+          for (int ww = 0; ww < 2; ++ww) {
+            // ring order K0 V0 K1 V1 ...; separate-P layout: K one block ahead,
+            // K0 K1 V0 K2 V1 ... K(n-1) V(n-2) V(n-1), so the MMA warp can issue
+            // S(j+1) before it needs V(j)
+            int j = jj, which = ww;
+            if constexpr (kSepP) {
+              const int i = 2 * jj + ww;
+              if (i == 0) { j = 0; which = 0; }
+              else if (i == 2 * n - 1) { j = n - 1; which = 1; }
+              else if (i & 1) { j = (i + 1) / 2; which = 0; }
+              else { j = i / 2 - 1; which = 1; }
+            }
             ptx::mbar_wait(&ctrl->kv_empty[kv_stage], kv_phase ^ 1);
             if constexpr (kCl > 1) {
               // this CTA's half of the block's rows, multicast into both CTAs
@@ -624,7 +635,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
         for (int j = 0; j < n; ++j) {
           ATTN_MSTAMP(0);
-          const int sV = take_slot();
           if (j + 1 < n) {
             sK = take_slot();
             ATTN_MSTAMP(1);
@@ -638,6 +648,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             __syncwarp();
           }
+          const int sV = take_slot();
 #pragma unroll
           for (int t = 0; t < 2; ++t) {
             const int nt = (t == 0) ? n0 : n1;
