@@ -111,7 +111,10 @@ struct Cfg {
 #ifndef ATTN_KV_STAGES
 #define ATTN_KV_STAGES 4
 #endif
-  static constexpr int kStages = (D == 128) ? ATTN_KV_STAGES : 8;  // K/V ring slots
+#ifndef ATTN_KV_STAGES_D64
+#define ATTN_KV_STAGES_D64 8
+#endif
+  static constexpr int kStages = (D == 128) ? ATTN_KV_STAGES : ATTN_KV_STAGES_D64;  // K/V ring slots
   static constexpr int kOffQ = 0;
   static constexpr int kOffKV = 2 * kQTileBytes;
   static constexpr int kOffCtrl = kOffKV + kStages * kKVBytes;
@@ -154,8 +157,8 @@ struct __align__(16) Ctrl {
   uint64_t sched_full[kSchedRing];
   uint64_t sched_empty[kSchedRing];
   uint64_t q_full, q_empty;
-  uint64_t kv_full[8];
-  uint64_t kv_empty[8];
+  uint64_t kv_full[16];
+  uint64_t kv_empty[16];
   uint64_t s_ready[2];
   uint64_t p_ready[2][4];   // [tile][slice of P]  softmax -> MMA
   uint64_t o_ready[2];
@@ -329,6 +332,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   Ctrl* ctrl = reinterpret_cast<Ctrl*>(smem + C::kOffCtrl);
   [[maybe_unused]] SplitRed* sred = reinterpret_cast<SplitRed*>(smem + C::kOffCtrl + 1024);
   static_assert(sizeof(Ctrl) <= 1024, "control block exceeds 1 KB");
+  static_assert(C::kStages <= 16, "K/V ring deeper than the Ctrl barrier arrays");
   static_assert(kSplit == 1 || C::kCtrlBytes >= 1024 + (int)sizeof(SplitRed), "split reductions do not fit");
   static_assert(C::kSmemBytes <= 232448, "shared memory exceeds 227 KB");
 
