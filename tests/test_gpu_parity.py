@@ -85,11 +85,14 @@ def _sample_rows(B, Hq, N, n, seed):
     return np.array(rows, dtype=np.int64)
 
 
-# BASELINE.json configs 2-4 at full size (config 5 in test_gpu_large), sampled rows.
+# BASELINE.json configs 2-4 (config 5 in test_gpu_large) and workload C6 at full size, sampled rows.
 FULL = [
     ("C2", 1, 32, 32, 8192, 128, False),
     ("C3", 1, 128, 128, 32768, 128, True),
     ("C4", 2, 64, 8, 16384, 128, True),
+    # NEXT-2 workload C6, DeepSeek-V3 prefill: d = 56 runs the d <= 64
+    # kernel (P in its own TMEM columns, K one block ahead of V)
+    ("C6", 1, 128, 128, 32768, 56, True),
 ]
 
 
