@@ -337,7 +337,23 @@ def measure_replicated(api, pdist, qkvo, shard, full_shape, causal, scale, mappi
     import torch.distributed as tdist
 
     q, k, v, o = qkvo
-    po = pdist.PeerOutput(full_shape, rank, world, dev)
+
+    def agree(ok):
+        # every rank learns whether all ranks succeeded, so a failure on one
+        # rank never leaves the others waiting in a collective below
+        t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MIN)
+        return bool(t.item())
+
+    po, err = None, None
+    try:
+        po = pdist.PeerOutput(full_shape, rank, world, dev)
+    except Exception as e:  # noqa: BLE001
+        err = repr(e)[:300]
+    if not agree(err is None):
+        if po is not None:
+            po.close()
+        return {"error": err or "PeerOutput failed on another rank"}
     dsts = [po.ptrs[rank]] + [p for r, p in enumerate(po.ptrs) if r != rank]
     nccl = tdist.get_backend() == "nccl"
     gbuf = torch.empty((world,) + tuple(o.shape), dtype=o.dtype, device=dev) if nccl else None
@@ -345,6 +361,15 @@ def measure_replicated(api, pdist, qkvo, shard, full_shape, causal, scale, mappi
     def fused():
         api.attn_fwd_replicated(q, k, v, dsts, full_shape[1], shard.q_lo, causal=causal, scale=scale,
                                 mapping=mapping, stream=stream)
+
+    try:  # one checked call before the timed ones
+        fused()
+        torch.cuda.synchronize()
+    except Exception as e:  # noqa: BLE001
+        err = repr(e)[:300]
+    if not agree(err is None):
+        po.close()
+        return {"error": err or "attn_fwd_replicated failed on another rank"}
 
     def gathered():
         api.attn_fwd(q, k, v, o, causal=causal, scale=scale, mapping=mapping, stream=stream)
