@@ -264,22 +264,15 @@ def run_ours(a):
     else:
         # q, k, v, O, dO, lse host -> device; attn_bwd; dq, dk, dv device -> host
         ins_h = [t.cpu().pin_memory() for t in (*sets[0][:3], *bwd_inputs[0])]
-        ins_d = [torch.empty_like(t, device=dev) for t in ins_h]
-        outs_d = [torch.empty_like(ins_d[i]) for i in range(3)]
         outs_h = [torch.empty_like(ins_h[i]).pin_memory() for i in range(3)]
 
         def e2e_step():
-            for hsrc, ddst in zip(ins_h, ins_d):
-                ddst.copy_(hsrc, non_blocking=True)
-            qd, kd, vd, od, lsed, dod = ins_d
-            api.attn_bwd(qd, kd, vd, od, dod, lsed, causal=causal, scale=scale, mapping=a.mapping,
-                         dq=outs_d[0], dk=outs_d[1], dv=outs_d[2], stream=stream)
-            for dsrc, hdst in zip(outs_d, outs_h):
-                hdst.copy_(dsrc, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
+            qh_, kh_, vh_, oh_, lseh_, doh_ = ins_h
+            api.attn_bwd_host(qh_, kh_, vh_, oh_, doh_, lseh_, *outs_h, causal=causal, scale=scale,
+                              mapping=a.mapping, stream=stream)
         h2d = sum(t.numel() * t.element_size() for t in ins_h)
         d2h = sum(t.numel() * t.element_size() for t in outs_h)
-        e2e_api = "attn_bwd (pinned host q,k,v,O,dO,lse -> H2D + kernels + D2H of dq,dk,dv + sync)"
+        e2e_api = "attn_bwd_host (pinned host q,k,v,O,dO,lse; chunked H2D || kernels || D2H of dq,dk,dv; sync)"
     for _ in range(2):
         e2e_step()
     if world > 1:

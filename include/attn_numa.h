@@ -175,6 +175,22 @@ ATTN_API int attn_bwd(const void* q, const void* k, const void* v, const void* o
 ATTN_API int attn_fwd_host(const void* q_host, const void* k_host, const void* v_host, void* o_host, int B, int Hq,
                   int Hkv, int N, int d, int causal, float scale, int mapping, void* cuda_stream);
 
+/* End-to-end backward on HOST buffers (layouts as attn_bwd; lse is fp32
+ * [B][Hq][N]): copies q, k, v, o, dout, lse host->device into library-owned
+ * device buffers, runs attn_bwd's kernels, copies dq, dk, dv device->host and
+ * synchronises `cuda_stream` before returning.  Pipelined like attn_fwd_host
+ * (chunks of whole KV groups of one batch item on three library streams:
+ * H2D of chunk i+1 || backward of chunk i || D2H of chunk i-1); the gradients
+ * of different KV groups are independent (eq:ba), so the
+ * result is bit-identical to one attn_bwd call on device copies.  Host
+ * buffers should be pinned.  Errors as attn_bwd (ATTN_CLUSTER_MULTICAST is
+ * UNSUPPORTED); buffers are reused across calls and freed by attn_shutdown().
+ * Not reentrant across threads on one device. */
+ATTN_API int attn_bwd_host(const void* q_host, const void* k_host, const void* v_host, const void* o_host,
+                           const void* dout_host, const float* lse_host, void* dq_host, void* dk_host, void* dv_host,
+                           int B, int Hq, int Hkv, int N, int d, int causal, float scale, int mapping,
+                           void* cuda_stream);
+
 /* Head-sharded forward with REPLICATED output stored by the kernel itself
  * (the fused alternative to an all-gather of O; heads are
  * independent).  q, k, v are this rank's shard ([B][Hq][N][d],

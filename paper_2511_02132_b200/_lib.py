@@ -16,7 +16,7 @@ ATTN_MAX_SMID = 512
 
 # every symbol include/attn_numa.h declares (checked by tests/test_boundary.py)
 EXPORTS = (
-    "attn_fwd", "attn_fwd_stream", "attn_fwd_lse", "attn_bwd", "attn_fwd_host", "attn_set_stream", "attn_init", "attn_topology",
+    "attn_fwd", "attn_fwd_stream", "attn_fwd_lse", "attn_bwd", "attn_fwd_host", "attn_bwd_host", "attn_set_stream", "attn_init", "attn_topology",
     "attn_set_topology_override", "attn_set_schedule_trace", "attn_schedule_order",
     "attn_last_launch_info", "attn_status_string", "attn_last_error", "attn_version", "attn_shutdown",
     "attn_fwd_replicated", "attn_ipc_get_handle", "attn_ipc_open", "attn_ipc_close",
@@ -76,6 +76,7 @@ def load():
     lib.attn_fwd_host.argtypes = fwd_args + [vp]
     lib.attn_fwd_lse.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, i32, i32, i32, f32, i32, vp]
     lib.attn_bwd.argtypes = [vp] * 9 + [i32, i32, i32, i32, i32, i32, f32, i32, vp]
+    lib.attn_bwd_host.argtypes = [vp] * 9 + [i32, i32, i32, i32, i32, i32, f32, i32, vp]
     lib.attn_set_stream.argtypes = [vp]
     lib.attn_init.argtypes = [i32]
     lib.attn_topology.argtypes = [i32, ctypes.POINTER(Topology)]
@@ -87,7 +88,7 @@ def load():
     lib.attn_ipc_get_handle.argtypes = [vp, ctypes.POINTER(IpcHandle)]
     lib.attn_ipc_open.argtypes = [ctypes.POINTER(IpcHandle), ctypes.POINTER(ctypes.c_void_p)]
     lib.attn_ipc_close.argtypes = [vp]
-    for f in ("attn_fwd", "attn_fwd_stream", "attn_fwd_lse", "attn_bwd", "attn_fwd_host", "attn_set_stream", "attn_init", "attn_topology",
+    for f in ("attn_fwd", "attn_fwd_stream", "attn_fwd_lse", "attn_bwd", "attn_fwd_host", "attn_bwd_host", "attn_set_stream", "attn_init", "attn_topology",
               "attn_set_topology_override", "attn_set_schedule_trace", "attn_schedule_order",
               "attn_last_launch_info", "attn_fwd_replicated", "attn_ipc_get_handle", "attn_ipc_open",
               "attn_ipc_close"):

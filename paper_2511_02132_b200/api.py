@@ -179,6 +179,27 @@ def attn_bwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor,
     return dq, dk, dv
 
 
+def attn_bwd_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor, dout: torch.Tensor,
+                  lse: torch.Tensor, dq: torch.Tensor, dk: torch.Tensor, dv: torch.Tensor, *, causal: bool = False,
+                  scale: Optional[float] = None, mapping="swizzled_head_first", order: str = "ascending",
+                  stream: Optional[torch.cuda.Stream] = None):
+    """End-to-end backward on HOST (ideally pinned) tensors: H2D of q, k, v, o,
+    dout (bf16) and lse (fp32), the backward kernels, D2H of dq, dk, dv, sync."""
+    for name, t in (("q", q), ("k", k), ("v", v), ("o", o), ("dout", dout), ("dq", dq), ("dk", dk), ("dv", dv)):
+        if t.is_cuda or t.dtype != torch.bfloat16 or not t.is_contiguous():
+            raise ValueError(f"attn_bwd_host takes contiguous bf16 CPU tensors ({name})")
+    if lse.is_cuda or lse.dtype != torch.float32 or not lse.is_contiguous():
+        raise ValueError("attn_bwd_host takes a contiguous float32 CPU lse")
+    B, Hq, N, d = q.shape
+    if scale is None:
+        scale = 1.0 / math.sqrt(d)
+    lib = _lib.load()
+    _check(lib.attn_bwd_host(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), dout.data_ptr(),
+                             lse.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), B, Hq, k.shape[1], N, d,
+                             int(bool(causal)), float(scale), _mapping_id(mapping, order), _stream_ptr(stream)))
+    return dq, dk, dv
+
+
 def attn_fwd_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor, *, causal: bool = False,
                   scale: Optional[float] = None, mapping="swizzled_head_first", order: str = "ascending",
                   stream: Optional[torch.cuda.Stream] = None, cluster: bool = False) -> torch.Tensor:

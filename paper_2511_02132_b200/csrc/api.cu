@@ -69,6 +69,9 @@ struct DevState {
   // e2e host-buffer path
   void* hbuf[4] = {nullptr, nullptr, nullptr, nullptr};
   size_t hbuf_bytes[4] = {0, 0, 0, 0};
+  // backward host-buffer path: q k v o dO lse dq dk dv
+  void* bbuf[9] = {};
+  size_t bbuf_bytes[9] = {};
   bool e2e_ready = false;
   float* dvec = nullptr;       // backward workspace: rowsum(dO o O)
   size_t dvec_elems = 0;
@@ -839,6 +842,93 @@ int attn_fwd_host(const void* q_host, const void* k_host, const void* v_host, vo
   return ATTN_OK;
 }
 
+int attn_bwd_host(const void* q_host, const void* k_host, const void* v_host, const void* o_host,
+                  const void* dout_host, const float* lse_host, void* dq_host, void* dk_host, void* dv_host, int B,
+                  int Hq, int Hkv, int N, int d, int causal, float scale, int mapping, void* cuda_stream) {
+  if (!q_host || !k_host || !v_host || !o_host || !dout_host || !lse_host || !dq_host || !dk_host || !dv_host)
+    return fail(ATTN_ERR_INVALID_VALUE, "null pointer");
+  if (B <= 0 || Hq <= 0 || Hkv <= 0 || N <= 0 || d <= 0) return fail(ATTN_ERR_INVALID_VALUE, "size <= 0");
+  if (Hq % Hkv != 0) return fail(ATTN_ERR_INVALID_VALUE, "Hq % Hkv != 0 (non-uniform GQA groups)");
+  if (mapping & ATTN_CLUSTER_MULTICAST) return fail(ATTN_ERR_UNSUPPORTED, "ATTN_CLUSTER_MULTICAST is forward-only");
+  int dev = 0;
+  int rc = current_device(dev);
+  if (rc != ATTN_OK) return rc;
+  DevState& st = g_dev[dev];
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(cuda_stream);
+  const int G = Hq / Hkv;
+  const size_t row_bytes = (size_t)N * d * 2, lrow_bytes = (size_t)N * 4;
+  const size_t nq = (size_t)B * Hq * row_bytes, nk = (size_t)B * Hkv * row_bytes, nl = (size_t)B * Hq * lrow_bytes;
+  const size_t need[9] = {nq, nk, nk, nq, nq, nl, nq, nk, nk};
+  {
+    std::lock_guard<std::mutex> lk(st.mu);
+    for (int i = 0; i < 9; ++i) {
+      if (st.bbuf_bytes[i] < need[i]) {
+        if (st.bbuf[i]) cudaFree(st.bbuf[i]);
+        st.bbuf[i] = nullptr;
+        st.bbuf_bytes[i] = 0;
+        ATTN_CUDA(cudaMalloc(&st.bbuf[i], need[i]));
+        st.bbuf_bytes[i] = need[i];
+      }
+    }
+    if (!st.e2e_ready) {
+      for (int i = 0; i < 3; ++i) ATTN_CUDA(cudaStreamCreateWithFlags(&st.e2e_stream[i], cudaStreamNonBlocking));
+      for (int i = 0; i < kE2EChunks + 1; ++i)
+        for (int j = 0; j < 2; ++j) ATTN_CUDA(cudaEventCreateWithFlags(&st.e2e_ev[j][i], cudaEventDisableTiming));
+      st.e2e_ready = true;
+    }
+  }
+  // Same pipeline as attn_fwd_host: chunks of whole KV groups of one batch
+  // item (the gradients of different KV groups are independent), H2D of chunk
+  // i+1 || the three backward kernels of chunk i || D2H of chunk i-1.
+  const size_t total = 4 * nq + 4 * nk + nl;
+  int target = (int)std::min<size_t>(kE2EChunks, std::max<size_t>(1, total / ((size_t)ATTN_E2E_CHUNK_MB << 20)));
+  const int tg = B * Hkv;
+  target = std::min(target, tg);
+  int gpc = (tg + target - 1) / target;  // KV groups per chunk
+  gpc = std::min(gpc, Hkv);
+  cudaStream_t cin = st.e2e_stream[0], comp = st.e2e_stream[1], cout = st.e2e_stream[2];
+  cudaEvent_t* ev_in = st.e2e_ev[0];
+  cudaEvent_t* ev_k = st.e2e_ev[1];
+  ATTN_CUDA(cudaEventRecord(ev_in[kE2EChunks], s));  // order after the caller's prior work
+  for (cudaStream_t x : {cin, comp, cout}) ATTN_CUDA(cudaStreamWaitEvent(x, ev_in[kE2EChunks], 0));
+  char* b[9];
+  for (int i = 0; i < 9; ++i) b[i] = static_cast<char*>(st.bbuf[i]);
+  const char* hin[6] = {static_cast<const char*>(q_host), static_cast<const char*>(k_host),
+                        static_cast<const char*>(v_host), static_cast<const char*>(o_host),
+                        static_cast<const char*>(dout_host), reinterpret_cast<const char*>(lse_host)};
+  char* hout[3] = {static_cast<char*>(dq_host), static_cast<char*>(dk_host), static_cast<char*>(dv_host)};
+  int c = 0;
+  for (int bi = 0; bi < B; ++bi) {
+    for (int g0 = 0; g0 < Hkv; g0 += gpc, ++c) {
+      const int gn = std::min(gpc, Hkv - g0);
+      const size_t qoff = ((size_t)bi * Hq + (size_t)g0 * G) * row_bytes, qlen = (size_t)gn * G * row_bytes;
+      const size_t koff = ((size_t)bi * Hkv + g0) * row_bytes, klen = (size_t)gn * row_bytes;
+      const size_t loff = ((size_t)bi * Hq + (size_t)g0 * G) * lrow_bytes, llen = (size_t)gn * G * lrow_bytes;
+      const size_t off[6] = {qoff, koff, koff, qoff, qoff, loff}, len[6] = {qlen, klen, klen, qlen, qlen, llen};
+      const int e = c % kE2EChunks;
+      if (c >= kE2EChunks) ATTN_CUDA(cudaStreamWaitEvent(cin, ev_k[e], 0));  // the event slot's previous chunk ran
+      for (int i = 0; i < 6; ++i)
+        ATTN_CUDA(cudaMemcpyAsync(b[i] + off[i], hin[i] + off[i], len[i], cudaMemcpyHostToDevice, cin));
+      ATTN_CUDA(cudaEventRecord(ev_in[e], cin));
+      ATTN_CUDA(cudaStreamWaitEvent(comp, ev_in[e], 0));
+      rc = bwd_impl(b[0] + qoff, b[1] + koff, b[2] + koff, b[3] + qoff, b[4] + qoff,
+                    reinterpret_cast<const float*>(b[5] + loff), b[6] + qoff, b[7] + koff, b[8] + koff, 1, gn * G, gn,
+                    N, d, causal, scale, mapping, comp);
+      if (rc != ATTN_OK) return rc;
+      ATTN_CUDA(cudaEventRecord(ev_k[e], comp));
+      ATTN_CUDA(cudaStreamWaitEvent(cout, ev_k[e], 0));
+      ATTN_CUDA(cudaMemcpyAsync(hout[0] + qoff, b[6] + qoff, qlen, cudaMemcpyDeviceToHost, cout));
+      ATTN_CUDA(cudaMemcpyAsync(hout[1] + koff, b[7] + koff, klen, cudaMemcpyDeviceToHost, cout));
+      ATTN_CUDA(cudaMemcpyAsync(hout[2] + koff, b[8] + koff, klen, cudaMemcpyDeviceToHost, cout));
+    }
+  }
+  ATTN_CUDA(cudaEventRecord(ev_k[kE2EChunks], cout));
+  ATTN_CUDA(cudaStreamWaitEvent(s, ev_k[kE2EChunks], 0));
+  ATTN_CUDA(cudaStreamSynchronize(s));
+  g_info.kernel_launches = 3 * c;  // D, dQ and dK/dV kernels per chunk
+  return ATTN_OK;
+}
+
 int attn_set_stream(void* cuda_stream) {
   g_stream = reinterpret_cast<cudaStream_t>(cuda_stream);
   return ATTN_OK;
@@ -970,7 +1060,7 @@ void attn_shutdown(void) {
   for (int dv = 0; dv < kMaxDevices; ++dv) {
     DevState& st = g_dev[dv];
     std::lock_guard<std::mutex> lk(st.mu);
-    if (!st.init && !st.hbuf[0]) continue;
+    if (!st.init && !st.hbuf[0] && !st.bbuf[0]) continue;
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(dv);
@@ -986,6 +1076,11 @@ void attn_shutdown(void) {
     st.d_domain = nullptr;
     st.d_counters = nullptr;
     for (int i = 0; i < 4; ++i) { st.hbuf[i] = nullptr; st.hbuf_bytes[i] = 0; }
+    for (int i = 0; i < 9; ++i) {
+      if (st.bbuf[i]) cudaFree(st.bbuf[i]);
+      st.bbuf[i] = nullptr;
+      st.bbuf_bytes[i] = 0;
+    }
     if (st.e2e_ready) {
       for (int i = 0; i < 3; ++i) cudaStreamDestroy(st.e2e_stream[i]);
       for (int j = 0; j < 2; ++j)

@@ -63,3 +63,27 @@ def test_backward_bitexact_across_mappings():
         torch.cuda.synchronize()
         for a, b in zip(got, ref):
             assert torch.equal(a.view(torch.int16), b.view(torch.int16)), m
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,N,d,causal", [
+    (1, 4, 2, 300, 128, True),      # one chunk
+    (2, 16, 8, 8192, 128, True),    # several pipelined chunks (>= 48 MB moved)
+    (1, 4, 4, 640, 56, False),      # head dim <= 64
+])
+def test_bwd_host_path_bitexact(B, Hq, Hkv, N, d, causal):
+    """attn_bwd_host (pinned host buffers, chunked H2D || kernels || D2H) gives
+    the same bits as attn_bwd on device copies (KV groups are independent)."""
+    from paper_2511_02132_b200 import attn_bwd_host, attn_last_launch_info
+
+    q, k, v = synth.make_qkv(B, Hq, Hkv, N, d, base=31, device="cuda")
+    do = synth.make_tensor("q", B, Hq, N, d, base=32, device="cuda")
+    o, lse = attn_fwd_lse(q, k, v, causal=causal)
+    dq, dk, dv = attn_bwd(q, k, v, o, do, lse, causal=causal)
+    torch.cuda.synchronize()
+    hin = [t.cpu().pin_memory() for t in (q, k, v, o, do, lse)]
+    hout = [torch.empty_like(t).pin_memory() for t in hin[:3]]
+    attn_bwd_host(*hin, *hout, causal=causal)
+    if N >= 8192:
+        assert attn_last_launch_info()["kernel_launches"] > 3  # more than one chunk
+    for name, got, ref in (("dq", hout[0], dq), ("dk", hout[1], dk), ("dv", hout[2], dv)):
+        assert torch.equal(got.view(torch.int16), ref.cpu().view(torch.int16)), name
