@@ -3,7 +3,8 @@
 Tolerance: gradients are bf16 outputs of
 bf16 P / dS operands with fp32 accumulation, so errors scale with the
 gradient's own magnitude: max |g - g_ref| <= 2e-2 * max(1, max|g_ref|) and
-mean |g - g_ref| <= 2e-3 * max(1, mean|g_ref|) per tensor.  The row LSE from
+mean |g - g_ref| <= 2e-3 * max(1, mean|g_ref|) + 2^-9 * mean|g_ref| per tensor
+(the last term is the gradient's own bf16 rounding, reading R21).  The row LSE from
 attn_fwd_lse: |lse - lse_ref| <= 1e-3.  Every mapping gives the same bits.
 """
 import math
@@ -25,7 +26,8 @@ def _check(name, got, ref):
     mx = max(1.0, np.abs(ref).max())
     mn = max(1.0, np.abs(ref).mean())
     assert err.max() <= 2e-2 * mx, f"{name}: max err {err.max():.3e} (ref max {np.abs(ref).max():.3e})"
-    assert err.mean() <= 2e-3 * mn, f"{name}: mean err {err.mean():.3e}"
+    # + the gradient's own bf16 rounding (reading R21)
+    assert err.mean() <= 2e-3 * mn + 2.0 ** -9 * np.abs(ref).mean(), f"{name}: mean err {err.mean():.3e}"
 
 
 CASES = [

@@ -26,7 +26,7 @@ def _cases(n, seed):
     out = []
     for _ in range(n):
         Hkv = rng.choice([1, 2, 3, 4])
-        G = rng.choice([1, 2, 4])
+        G = rng.choice([1, 2, 4, 8])
         N = rng.choice([1, 7, 128, 129, 255, 256, 300, rng.randint(1, 1500)])
         out.append(dict(B=rng.randint(1, 3), Hq=Hkv * G, Hkv=Hkv, N=N, d=8 * rng.randint(1, 16),
                         causal=rng.random() < 0.5, mapping=rng.choice(MAPS),
@@ -74,4 +74,5 @@ def test_backward_fuzz(case):
         e = np.abs(g.float().cpu().numpy() - r)
         assert np.isfinite(e).all(), name
         assert e.max() <= 2e-2 * max(1.0, np.abs(r).max()), (name, e.max())
-        assert e.mean() <= 2e-3 * max(1.0, np.abs(r).mean()), (name, e.mean())
+        # + the gradient's own bf16 rounding (reading R21)
+        assert e.mean() <= 2e-3 * max(1.0, np.abs(r).mean()) + 2.0 ** -9 * np.abs(r).mean(), (name, e.mean())
