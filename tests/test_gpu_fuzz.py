@@ -59,7 +59,10 @@ def test_forward_fuzz(case):
     assert np.isfinite(got).all() and err.max() <= MAX_TOL and err.mean() <= MEAN_TOL, (err.max(), err.mean())
 
 
-@pytest.mark.parametrize("case", [c for c in _cases(12, 77) if c["N"] <= 700],
+_N_BWD = int(os.environ.get("ATTN_FUZZ_BWD_CASES", "12"))
+
+
+@pytest.mark.parametrize("case", [c for c in _cases(_N_BWD, _SEED_FWD if _N_BWD != 12 else 77) if c["N"] <= 700],
                          ids=lambda c: "-".join(f"{k}{v}" for k, v in c.items()))
 def test_backward_fuzz(case):
     B, Hq, Hkv, N, d, causal = case["B"], case["Hq"], case["Hkv"], case["N"], case["d"], case["causal"]
