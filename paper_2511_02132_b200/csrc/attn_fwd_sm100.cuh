@@ -55,10 +55,6 @@ constexpr int kBlockN = 128;  // keys per K/V block
 #define ATTN_P_PARTS 2
 #endif
 constexpr int kPParts = ATTN_P_PARTS;
-// Speculative block max (experiment, off: measured slower)
-#ifndef ATTN_SPEC_MAX
-#define ATTN_SPEC_MAX 0
-#endif
 // Head dim <= 64 (plain CTAs): P gets its own TMEM columns (the 128 that
 // S0 S1 O0 O1 leave free) instead of aliasing S, so S_t(j+1) is issued as soon
 // as the softmax has loaded S_t(j) into registers and each tile's softmax runs
@@ -856,80 +852,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = 0; k < kCols; ++k)
             if (k > lim) r[k] = 0xff800000u;
         }
-#if ATTN_SPEC_MAX
-        // Speculative block (j > 0, no masked keys): the threshold rule keeps
-        // m_use = m for every row whose block max stays within kRescaleThreshold
-        // of m, so half 0 of P is exponentiated against m while the block max
-        // is formed; if any row of the warp moves the max beyond the threshold,
-        // S is reloaded from TMEM (nothing has been written over it yet) and
-        // the block takes the general path below.  Bit-identical to it.
-        if constexpr (kSplit == 1 && kPParts == 2 && !kSepP) {
-          if (j > 0 && !diag) {
-            const float negm = -m * c;
-            float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-            float2 sq[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
-                            make_float2(0.f, 0.f)};
-            auto exp_pair = [&](int k) {
-              const float2 x = ptx::ffma2(make_float2(__uint_as_float(r[k]), __uint_as_float(r[k + 1])), c, negm);
-              float2 pr;
-              constexpr int kEP = emu_period<D>();
-              if (kEP > 0 && ((k >> 1) % (kEP > 0 ? kEP : 1)) == kEP - 1) {
-                pr = ptx::ex2_poly2(x);
-              } else {
-                pr.x = ptx::ex2(x.x);
-                pr.y = ptx::ex2(x.y);
-              }
-              sq[(k >> 1) & 3] = ptx::fadd2(sq[(k >> 1) & 3], pr);
-              r[k >> 1] = ptx::pack_bf16(pr.x, pr.y);
-            };
-#pragma unroll
-            for (int k = 0; k < 64; k += 8) {
-#pragma unroll
-              for (int g4 = 0; g4 < 4; ++g4) {
-                mq[g4] = fmaxf(mq[g4], fmaxf(__uint_as_float(r[k + 2 * g4]), __uint_as_float(r[k + 2 * g4 + 1])));
-                exp_pair(k + 2 * g4);
-              }
-            }
-#pragma unroll
-            for (int k = 64; k < 128; k += 8) {
-#pragma unroll
-              for (int g4 = 0; g4 < 4; ++g4)
-                mq[g4] = fmaxf(mq[g4], fmaxf(__uint_as_float(r[k + 2 * g4]), __uint_as_float(r[k + 2 * g4 + 1])));
-            }
-            const float mxs = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
-#ifdef ATTN_TIMELINE
-            if (tl2) tl2[2] = clock64() + (long long)(mxs == 12345.f);
-#endif
-            if (!__any_sync(0xffffffffu, (mxs - m) * c > kRescaleThreshold)) {
-#pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                if (h == 1) {
-#pragma unroll
-                  for (int k = 64; k < 128; k += 2) exp_pair(k);
-                }
-#ifdef ATTN_TIMELINE
-                if (tl2) tl2[6 + h] = clock64() + (long long)(r[h * 32] == 12345u);
-#endif
-                ptx::tmem_st32(trow + colP + h * 32, r + h * 32);
-                ptx::tmem_wait_st();
-                ptx::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&ctrl->p_ready[t][h]);
-#ifdef ATTN_TIMELINE
-                if (tls) tls[1 + h] = clock64();
-                if (tl2) tl2[3 + h] = clock64();
-#endif
-              }
-              const float2 s01 = ptx::fadd2(sq[0], sq[1]), s23 = ptx::fadd2(sq[2], sq[3]);
-              const float2 s4 = ptx::fadd2(s01, s23);
-              l = fmaf(l, 1.f, s4.x + s4.y);
-              continue;
-            }
-            // the max moved: reload S (intact in TMEM) and take the general path
-            ptx::tmem_ld128(trow + colS, r);
-          }
-        }
-#endif
         // row max: four independent FMNMX3 chains, then across the kSplit warps
         float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
