@@ -75,6 +75,19 @@ def load_profile_summary(workload, mapping, cluster=False):
         return None
 
 
+def ncu_fields(prof):
+    """Per-mapping ncu evidence (north star: L2 hit rate, tensor-pipe
+    utilisation, HBM GB/s) from a committed --set full summary, or None."""
+    if not prof:
+        return {"l2_hit_rate_pct": None, "tensor_pipe_pct": None, "hbm_gbs": None, "dram_gb_per_launch": None}
+    t = prof.get("gpu__time_duration.sum")
+    dram = prof.get("dram_bytes_per_launch")
+    return {"l2_hit_rate_pct": prof.get("lts__t_sector_hit_rate.pct"),
+            "tensor_pipe_pct": prof.get("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"),
+            "hbm_gbs": round(dram / t / 1e9, 1) if (dram and t) else None,
+            "dram_gb_per_launch": round(dram / 1e9, 3) if dram else None}
+
+
 # ----------------------------------------------------------------- clocks
 class ClockSampler:
     """NVML SM clock + throttle reasons sampled in a thread during the timed region."""
@@ -224,7 +237,7 @@ def run_ours(a):
             msm, _, _ = timed(m, max(3, a.steps // 4), 2)
         prof = load_profile_summary(a.workload, m, bool(a.cluster)) if a.pass_ == "fwd" else None
         by_mapping[m] = {"tflops": round(flops_job / (msm * 1e-3) / 1e12, 1), "ms_per_step": round(msm, 4),
-                         "l2_hit_rate_pct": prof.get("lts__t_sector_hit_rate.pct") if prof else None}
+                         **(ncu_fields(prof) if a.pass_ == "fwd" else {})}
         if a.pass_ == "fwd":
             cluster_on[0] = 1 - a.cluster
             msc, _, _ = timed(m, max(3, a.steps // 4), 2)
@@ -232,10 +245,7 @@ def run_ours(a):
             profc = load_profile_summary(a.workload, m, not a.cluster)
             by_mapping[m]["cluster" if not a.cluster else "no_cluster"] = {
                 "tflops": round(flops_job / (msc * 1e-3) / 1e12, 1), "ms_per_step": round(msc, 4),
-                "l2_hit_rate_pct": profc.get("lts__t_sector_hit_rate.pct") if profc else None,
-                "dram_gb_per_launch": round(profc["dram_bytes_per_launch"] / 1e9, 3) if profc else None}
-            if prof:
-                by_mapping[m]["dram_gb_per_launch"] = round(prof["dram_bytes_per_launch"] / 1e9, 3)
+                **ncu_fields(profc)}
 
     # replicated output (N > 1, forward): the kernel epilogue storing O into
     # every rank's buffer over NVLink (attn_fwd_replicated + CUDA IPC) vs the
