@@ -165,3 +165,33 @@ def test_host_buffer_pipelined_chunks_bitexact():
     attn_fwd_host(qh, kh, vh, oh, causal=True)
     assert attn_last_launch_info()["kernel_launches"] > 1
     assert torch.equal(od.cpu().view(torch.int16), oh.view(torch.int16))
+
+
+def test_shutdown_then_reuse():
+    """attn_shutdown() frees every library buffer (device state, host-path
+    staging of forward and backward); the next call re-initialises and gives
+    the same bits."""
+    from paper_2511_02132_b200 import attn_bwd_host, attn_fwd_lse, attn_shutdown
+
+    q, k, v = synth.make_qkv(1, 4, 2, 384, 128, base=41, device="cuda")
+    ref = attn_fwd(q, k, v, causal=True)
+    qh, kh, vh = (t.cpu().pin_memory() for t in (q, k, v))
+    oh = torch.empty_like(qh).pin_memory()
+    attn_fwd_host(qh, kh, vh, oh, causal=True)
+    o, lse = attn_fwd_lse(q, k, v, causal=True)
+    do = synth.make_tensor("q", 1, 4, 384, 128, base=42, device="cuda")
+    hin = [t.cpu().pin_memory() for t in (q, k, v, o, do, lse)]
+    g1 = [torch.empty_like(t).pin_memory() for t in hin[:3]]
+    attn_bwd_host(*hin, *g1, causal=True)
+    torch.cuda.synchronize()
+    attn_shutdown()
+    o2 = attn_fwd(q, k, v, causal=True)
+    oh2 = torch.empty_like(qh).pin_memory()
+    attn_fwd_host(qh, kh, vh, oh2, causal=True)
+    g2 = [torch.empty_like(t).pin_memory() for t in hin[:3]]
+    attn_bwd_host(*hin, *g2, causal=True)
+    torch.cuda.synchronize()
+    assert torch.equal(o2.view(torch.int16), ref.view(torch.int16))
+    assert torch.equal(oh2.view(torch.int16), oh.view(torch.int16))
+    for a, b in zip(g1, g2):
+        assert torch.equal(a.view(torch.int16), b.view(torch.int16))
