@@ -1009,6 +1009,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     if (ATTN_SETMAXNREG) ptx::setmaxnreg_dec<kOtherRegs>();  // warp 3: idle
+#ifdef ATTN_TIMELINE
+    // timeline probe: when does each s_ready[0] phase (S_0(j) of the first
+    // unit) complete?  -> trace[3072 + j]
+    if (p.trace && blockIdx.x == 0 && lane == 0) {
+      long long* tq = reinterpret_cast<long long*>(p.trace) + 3072;
+      for (int k = 0; k < 64; ++k) {
+        uint32_t ok = 0;
+        while (!ok) {
+          asm volatile(
+              "{\n\t.reg .pred q;\n\t"
+              "mbarrier.test_wait.parity.acquire.cta.shared::cta.b64 q, [%1], %2;\n\t"
+              "selp.u32 %0, 1, 0, q;\n\t}"
+              : "=r"(ok)
+              : "r"(ptx::smem_u32(&ctrl->s_ready[0])), "r"((uint32_t)(k & 1))
+              : "memory");
+        }
+        tq[k] = clock64();
+      }
+    }
+#endif
   }
 
   ptx::tc_fence_before();

@@ -46,3 +46,7 @@ sf = t[2048 + 512: 2048 + 512 + 128].reshape(64, 2)
 print(" j | s_free ok (tile 0, tile 1) relative to tile 0 s_wake of block j")
 for j in range(8, 16):
     print(f"{j:2d} | " + " ".join(f"{x - sm[0][j, 0]:7d}" for x in sf[j]))
+done = t[3072: 3072 + 64]
+print(" j | s_ready[0] phase j+1 complete (S_0(j+1) landed), relative to tile 0 s_wake of block j; next s_wake")
+for j in range(8, 16):
+    print(f"{j:2d} | {done[j + 1] - sm[0][j, 0]:7d}  {sm[0][j + 1, 0] - sm[0][j, 0]:7d}")
