@@ -286,7 +286,7 @@ __device__ __forceinline__ void run_scheduler(const KernelParams& p, CT* ctrl) {
       ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&ctrl->sched_full[stage]), 1));
     }
     if (qi < 0) break;
-#if !defined(ATTN_PROFILE_WAITS) && !defined(ATTN_TIMELINE)
+#if !defined(ATTN_PROFILE_WAITS) && !defined(ATTN_TIMELINE) && !defined(ATTN_CYCLES)
     if (kCl == 1 && p.trace) {
       const long long id = ((long long)b * p.Hq + h) * p.U + u;
       if (id < p.trace_cap) {
@@ -784,6 +784,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
     SchedReader<kCl> sr;
     uint32_t s_phase = 0, o_phase = 0, gblk = 0;
+#ifdef ATTN_CYCLES
+    // per-warp cycle account of the softmax chain, kept in registers and
+    // written once at exit: [S wait, ld, max, exps+stores, p_free wait,
+    // epilogue (incl. o_ready wait), o_ready wait, blocks]
+    long long cyc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long c_t = 0;
+#define ATTN_CYC_START() c_t = clock64();
+#define ATTN_CYC_ADD(i) { const long long c_n = clock64(); cyc[i] += c_n - c_t; c_t = c_n; }
+#else
+#define ATTN_CYC_START()
+#define ATTN_CYC_ADD(i)
+#endif
     [[maybe_unused]] uint32_t pf_phase = 0;
     while (true) {
       const int4 e = sr.next(ctrl, false);
@@ -805,7 +817,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
       float m = -INFINITY, l = 0.f;
       for (int j = 0; j < nt; ++j, ++gblk) {
+        ATTN_CYC_START();
         ptx::mbar_wait(&ctrl->s_ready[t], s_phase);
+        ATTN_CYC_ADD(0);
         s_phase ^= 1;
         ptx::tc_fence_after();
 #ifdef ATTN_TIMELINE
@@ -852,6 +866,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = 0; k < kCols; ++k)
             if (k > lim) r[k] = 0xff800000u;
         }
+        ATTN_CYC_ADD(1);
         // row max: four independent FMNMX3 chains, then across the kSplit warps
         float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
@@ -931,7 +946,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if constexpr (kSepP) {
             if (h == 0 && j > 0) {  // PV_t(j-1) has finished reading P_t and adding into O_t
+              ATTN_CYC_ADD(3);
               ptx::mbar_wait(&ctrl->p_free[t], pf_phase);
+              ATTN_CYC_ADD(4);
               pf_phase ^= 1;
               ptx::tc_fence_after();
               if (any_rescale) fixup();
@@ -956,6 +973,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
         }
         };
+        ATTN_CYC_ADD(2);
         if (diag) exp_block(std::true_type{});
         else exp_block(std::false_type{});
         const float2 s01 = ptx::fadd2(sq[0], sq[1]), s23 = ptx::fadd2(sq[2], sq[3]);
@@ -966,14 +984,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float sum = s4.x + s4.y;
         l = (j == 0) ? sum : fmaf(l, alpha, sum);
         m = m_use;
+        ATTN_CYC_ADD(3);
+#ifdef ATTN_CYCLES
+        cyc[7] += 1;
+#endif
       }
+      ATTN_CYC_START();
       // ---- epilogue: O / l -> bf16 -> global
       if constexpr (kSplit == 2) {
         sred->lsum[t][quarter][hf][lane] = l;
         ptx::named_bar_sync(bar_id, 64);
         l += sred->lsum[t][quarter][hf ^ 1][lane];
       }
-      ptx::mbar_wait(&ctrl->o_ready[t], o_phase);
+      {
+#ifdef ATTN_CYCLES
+        const long long c_o = clock64();
+#endif
+        ptx::mbar_wait(&ctrl->o_ready[t], o_phase);
+#ifdef ATTN_CYCLES
+        cyc[6] += clock64() - c_o;
+#endif
+      }
       o_phase ^= 1;
       ptx::tc_fence_after();
       const float inv_l = 1.f / l;
@@ -1006,7 +1037,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       ptx::tc_fence_before();
+      ATTN_CYC_ADD(5);
     }
+#ifdef ATTN_CYCLES
+    if (p.trace && lane == 0 && blockIdx.x < 64) {
+      long long* out = reinterpret_cast<long long*>(p.trace) + (blockIdx.x * 8 + (warp - 4)) * 8;
+      for (int i = 0; i < 8; ++i) out[i] = cyc[i];
+    }
+#endif
   } else {
     if (ATTN_SETMAXNREG) ptx::setmaxnreg_dec<kOtherRegs>();  // warp 3: idle
 #ifdef ATTN_TIMELINE
