@@ -47,6 +47,17 @@
  *  - The library owns per-device workspace (die table, scheduler counters,
  *    probe buffers), created lazily under a mutex and released by
  *    attn_shutdown().
+ *  - Concurrency: launches are asynchronous on the caller's stream.  Each
+ *    stream gets its own slot of scheduler queue counters (the persistent
+ *    grid pops work with atomics on them and its last CTA re-zeroes them), so
+ *    any number of calls may be queued on one stream, and calls on up to 64
+ *    DIFFERENT streams of one device may be in flight at the same time.
+ *    Beyond 64 concurrently busy streams, or when a CUDA graph that captured
+ *    a launch is replayed on another stream while eager launches run on the
+ *    capture stream, two grids can share counters and skip or repeat work
+ *    units: serialise such launches.  attn_bwd's rowsum(dO o O) workspace is
+ *    allocated per call in stream order (cudaMallocAsync), so concurrent
+ *    backward calls on different streams are safe.
  */
 #ifndef ATTN_NUMA_H
 #define ATTN_NUMA_H
@@ -75,6 +86,17 @@ typedef enum {
  * (PAPER.md:226, :246).  Applied identically under every mapping; it changes
  * only the schedule, never the result bits. */
 #define ATTN_ORDER_DESCENDING 0x100
+
+/* OR into `mapping`: alternate the unit direction per die queue -- queue d
+ * visits each (b, h)'s units ascending if d is even, descending if d is odd
+ * (XOR-combined with ATTN_ORDER_DESCENDING).  Only the swizzled mappings have
+ * more than one queue; block-first / head-first are unaffected.  Purpose
+ * (B200 reading, R22): under swizzled head-first the two dies each
+ * stream one causal head, and a causal head's live K/V prefix grows with the
+ * unit index; running the dies in opposite directions keeps the SUM of the
+ * two live prefixes -- what the dies' shared L2 must hold -- near one head's
+ * K/V instead of two.  Schedule only: never changes the result bits. */
+#define ATTN_ORDER_ALTERNATE 0x400
 
 /* OR into `mapping` (forward only): run CTA pairs as thread-block clusters
  * (NEXT-4, the ACC idea one level down: "CTAs that share K/V

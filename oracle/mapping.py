@@ -204,6 +204,12 @@ def descending(queues: List[List[Tile]], nblk: int) -> List[List[Tile]]:
     return [[(b, h, nblk - 1 - k) for (b, h, k) in q] for q in queues]
 
 
+def alternate(queues: List[List[Tile]], nblk: int) -> List[List[Tile]]:
+    """The same queues with queue d's (b, h) blocks visited last-first when d
+    is odd (R22; a schedule knob, never part of the result)."""
+    return [q if d % 2 == 0 else [(b, h, nblk - 1 - k) for (b, h, k) in q] for d, q in enumerate(queues)]
+
+
 def is_bijection(queues: List[List[Tile]], B: int, Hq: int, nblk: int) -> bool:
     """every tile appears exactly once across the queues."""
     flat = [t for q in queues for t in q]

@@ -35,14 +35,15 @@ def _check(rc: int) -> None:
 
 ORDER_DESCENDING = 0x100  # include/attn_numa.h ATTN_ORDER_DESCENDING
 CLUSTER_MULTICAST = 0x200  # include/attn_numa.h ATTN_CLUSTER_MULTICAST
+ORDER_ALTERNATE = 0x400  # include/attn_numa.h ATTN_ORDER_ALTERNATE
+ORDERS = {"ascending": 0, "descending": ORDER_DESCENDING, "alternate": ORDER_ALTERNATE}
 
 
 def _mapping_id(mapping, order: str = "ascending", cluster: bool = False) -> int:
     m = mapping if isinstance(mapping, int) else MAPPINGS[str(mapping).lower()]
-    if order == "descending":
-        m |= ORDER_DESCENDING
-    elif order != "ascending":
-        raise ValueError("order must be 'ascending' or 'descending'")
+    if order not in ORDERS:
+        raise ValueError("order must be 'ascending', 'descending' or 'alternate'")
+    m |= ORDERS[order]
     if cluster:
         m |= CLUSTER_MULTICAST
     return m
@@ -51,6 +52,36 @@ def _mapping_id(mapping, order: str = "ascending", cluster: bool = False) -> int
 def _stream_ptr(stream: Optional[torch.cuda.Stream]) -> int:
     s = stream if stream is not None else torch.cuda.current_stream()
     return int(s.cuda_stream)
+
+
+def _check_tensor(name: str, t, shape, dtype=torch.bfloat16, cuda: bool = True) -> None:
+    """One tensor against the C-ABI layout: contiguous, `dtype`, exactly
+    `shape`, and on a CUDA device (cuda=True) or in host memory (cuda=False).
+    The library sizes every copy and TMA view from q's shape, so a smaller or
+    strided tensor would be read or written past its end."""
+    where = "CUDA" if cuda else "CPU"
+    if not isinstance(t, torch.Tensor) or t.dtype != dtype or bool(t.is_cuda) != cuda:
+        raise TypeError(f"{name} must be a {dtype} {where} tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous (row-major {list(shape)})")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} has shape {list(t.shape)}, expected {list(shape)}")
+
+
+def _qkv_shape(q, k, v, cuda: bool = True):
+    """Validate q [B, Hq, N, d], k and v [B, Hkv, N, d] (same B, N, d); returns (B, Hq, Hkv, N, d)."""
+    if not isinstance(q, torch.Tensor) or q.dim() != 4:
+        raise ValueError("q must be a [B, Hq, N, d] tensor")
+    if not isinstance(k, torch.Tensor) or k.dim() != 4:
+        raise ValueError("k must be a [B, Hkv, N, d] tensor")
+    B, Hq, N, d = q.shape
+    Hkv = k.shape[1]
+    _check_tensor("q", q, (B, Hq, N, d), cuda=cuda)
+    _check_tensor("k", k, (B, Hkv, N, d), cuda=cuda)
+    _check_tensor("v", v, (B, Hkv, N, d), cuda=cuda)
+    if cuda and not (k.device == q.device and v.device == q.device):
+        raise ValueError("q, k, v must be on one device")
+    return B, Hq, Hkv, N, d
 
 
 def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: Optional[torch.Tensor] = None, *,
@@ -66,19 +97,11 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: Optional[torc
     CTA pairs that multicast K/V (ATTN_CLUSTER_MULTICAST).  Results are
     bit-identical either way.
     """
-    for name, t in (("q", q), ("k", k), ("v", v)):
-        if not isinstance(t, torch.Tensor) or t.dtype != torch.bfloat16 or not t.is_cuda:
-            raise TypeError(f"{name} must be a bfloat16 CUDA tensor")
-        if t.dim() != 4 or not t.is_contiguous():
-            raise ValueError(f"{name} must be a contiguous [B, H, N, d] tensor")
-    B, Hq, N, d = q.shape
-    Hkv = k.shape[1]
-    if tuple(k.shape) != (B, Hkv, N, d) or tuple(v.shape) != tuple(k.shape):
-        raise ValueError("k, v must be [B, Hkv, N, d] matching q")
+    B, Hq, Hkv, N, d = _qkv_shape(q, k, v)
     if o is None:
         o = torch.empty_like(q)
-    elif o.dtype != torch.bfloat16 or not o.is_contiguous() or tuple(o.shape) != tuple(q.shape):
-        raise ValueError("o must be a contiguous bf16 tensor shaped like q")
+    else:
+        _check_tensor("o", o, q.shape)
     if scale is None:
         scale = 1.0 / math.sqrt(d)
     lib = _lib.load()
@@ -97,14 +120,13 @@ def attn_fwd_replicated(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o_dst
     q/k/v: this rank's shard; o_dst: full [B, Hq_out, N, d] outputs, given as
     bf16 CUDA tensors (this device) or raw device addresses (peer buffers
     mapped with ipc_open).  The shard's heads land at head_offset."""
-    B, Hq, N, d = q.shape
+    B, Hq, Hkv, N, d = _qkv_shape(q, k, v)
     if not 1 <= len(o_dst) <= 8:
         raise ValueError("1 to 8 destinations")
     ptrs = []
     for t in o_dst:
         if isinstance(t, torch.Tensor):
-            if t.dtype != torch.bfloat16 or not t.is_contiguous() or tuple(t.shape) != (B, Hq_out, N, d):
-                raise ValueError("each destination must be a contiguous bf16 [B, Hq_out, N, d] tensor")
+            _check_tensor("o_dst[i]", t, (B, int(Hq_out), N, d))
             ptrs.append(t.data_ptr())
         else:
             ptrs.append(int(t))
@@ -113,7 +135,7 @@ def attn_fwd_replicated(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o_dst
     arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
     lib = _lib.load()
     _check(lib.attn_fwd_replicated(q.data_ptr(), k.data_ptr(), v.data_ptr(), arr, len(ptrs), int(Hq_out),
-                                   int(head_offset), B, Hq, k.shape[1], N, d, int(bool(causal)), float(scale),
+                                   int(head_offset), B, Hq, Hkv, N, d, int(bool(causal)), float(scale),
                                    _mapping_id(mapping, order, cluster), _stream_ptr(stream)))
 
 
@@ -140,14 +162,14 @@ def attn_fwd_lse(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: b
                  scale: Optional[float] = None, mapping="swizzled_head_first", order: str = "ascending",
                  stream: Optional[torch.cuda.Stream] = None, cluster: bool = False):
     """Forward that also returns the fp32 row log-sum-exp [B, Hq, N] (backward input)."""
-    B, Hq, N, d = q.shape
+    B, Hq, Hkv, N, d = _qkv_shape(q, k, v)
     o = torch.empty_like(q)
     lse = torch.empty((B, Hq, N), dtype=torch.float32, device=q.device)
     if scale is None:
         scale = 1.0 / math.sqrt(d)
     lib = _lib.load()
     _check(lib.attn_fwd_lse(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), lse.data_ptr(), B, Hq,
-                            k.shape[1], N, d, int(bool(causal)), float(scale), _mapping_id(mapping, order, cluster),
+                            Hkv, N, d, int(bool(causal)), float(scale), _mapping_id(mapping, order, cluster),
                             _stream_ptr(stream)))
     return o, lse
 
@@ -158,23 +180,20 @@ def attn_bwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor,
              dq: Optional[torch.Tensor] = None, dk: Optional[torch.Tensor] = None, dv: Optional[torch.Tensor] = None):
     """Gradients (dq, dk, dv) of sum(dout * attention(q, k, v)) (PAPER.md eq:ba), bf16.
     dq / dk / dv may be passed as preallocated outputs (shaped like q / k / v)."""
-    for name, t in (("q", q), ("k", k), ("v", v), ("o", o), ("dout", dout)):
-        if t.dtype != torch.bfloat16 or not t.is_cuda or not t.is_contiguous():
-            raise TypeError(f"{name} must be a contiguous bfloat16 CUDA tensor")
-    if lse.dtype != torch.float32 or not lse.is_cuda or not lse.is_contiguous():
-        raise TypeError("lse must be a contiguous float32 CUDA tensor")
-    B, Hq, N, d = q.shape
+    B, Hq, Hkv, N, d = _qkv_shape(q, k, v)
+    _check_tensor("o", o, q.shape)
+    _check_tensor("dout", dout, q.shape)
+    _check_tensor("lse", lse, (B, Hq, N), dtype=torch.float32)
     dq = torch.empty_like(q) if dq is None else dq
     dk = torch.empty_like(k) if dk is None else dk
     dv = torch.empty_like(v) if dv is None else dv
     for name, t, ref in (("dq", dq, q), ("dk", dk, k), ("dv", dv, v)):
-        if t.shape != ref.shape or t.dtype != torch.bfloat16 or not t.is_cuda or not t.is_contiguous():
-            raise TypeError(f"{name} must be a contiguous bfloat16 CUDA tensor shaped like {name[1:]}")
+        _check_tensor(name, t, ref.shape)
     if scale is None:
         scale = 1.0 / math.sqrt(d)
     lib = _lib.load()
     _check(lib.attn_bwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), dout.data_ptr(), lse.data_ptr(),
-                        dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), B, Hq, k.shape[1], N, d, int(bool(causal)),
+                        dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), B, Hq, Hkv, N, d, int(bool(causal)),
                         float(scale), _mapping_id(mapping, order), _stream_ptr(stream)))
     return dq, dk, dv
 
@@ -185,17 +204,16 @@ def attn_bwd_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Te
                   stream: Optional[torch.cuda.Stream] = None):
     """End-to-end backward on HOST (ideally pinned) tensors: H2D of q, k, v, o,
     dout (bf16) and lse (fp32), the backward kernels, D2H of dq, dk, dv, sync."""
-    for name, t in (("q", q), ("k", k), ("v", v), ("o", o), ("dout", dout), ("dq", dq), ("dk", dk), ("dv", dv)):
-        if t.is_cuda or t.dtype != torch.bfloat16 or not t.is_contiguous():
-            raise ValueError(f"attn_bwd_host takes contiguous bf16 CPU tensors ({name})")
-    if lse.is_cuda or lse.dtype != torch.float32 or not lse.is_contiguous():
-        raise ValueError("attn_bwd_host takes a contiguous float32 CPU lse")
-    B, Hq, N, d = q.shape
+    B, Hq, Hkv, N, d = _qkv_shape(q, k, v, cuda=False)
+    for name, t, shape in (("o", o, q.shape), ("dout", dout, q.shape), ("dq", dq, q.shape), ("dk", dk, k.shape),
+                           ("dv", dv, k.shape)):
+        _check_tensor(name, t, shape, cuda=False)
+    _check_tensor("lse", lse, (B, Hq, N), dtype=torch.float32, cuda=False)
     if scale is None:
         scale = 1.0 / math.sqrt(d)
     lib = _lib.load()
     _check(lib.attn_bwd_host(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), dout.data_ptr(),
-                             lse.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), B, Hq, k.shape[1], N, d,
+                             lse.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), B, Hq, Hkv, N, d,
                              int(bool(causal)), float(scale), _mapping_id(mapping, order), _stream_ptr(stream)))
     return dq, dk, dv
 
@@ -204,11 +222,8 @@ def attn_fwd_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Te
                   scale: Optional[float] = None, mapping="swizzled_head_first", order: str = "ascending",
                   stream: Optional[torch.cuda.Stream] = None, cluster: bool = False) -> torch.Tensor:
     """End-to-end call on HOST (ideally pinned) bf16 tensors: H2D, kernel, D2H, sync."""
-    for t in (q, k, v, o):
-        if t.is_cuda or t.dtype != torch.bfloat16 or not t.is_contiguous():
-            raise ValueError("attn_fwd_host takes contiguous bf16 CPU tensors")
-    B, Hq, N, d = q.shape
-    Hkv = k.shape[1]
+    B, Hq, Hkv, N, d = _qkv_shape(q, k, v, cuda=False)
+    _check_tensor("o", o, q.shape, cuda=False)
     if scale is None:
         scale = 1.0 / math.sqrt(d)
     lib = _lib.load()

@@ -61,7 +61,10 @@ struct DevState {
   attn_topology_t active{};
   signed char* d_domain = nullptr;
   int* d_counters = nullptr;
-  unsigned slot = 0;
+  // counter slot of each stream that launched recently (see counter_slot)
+  cudaStream_t slot_stream[kCounterSlots] = {};
+  unsigned long long slot_used[kCounterSlots] = {};
+  unsigned long long slot_tick = 0;
   attn_trace_rec_t* trace = nullptr;
   long long trace_cap = 0;
   bool attr_done[8] = {false, false, false, false, false, false, false, false};
@@ -73,8 +76,6 @@ struct DevState {
   void* bbuf[9] = {};
   size_t bbuf_bytes[9] = {};
   bool e2e_ready = false;
-  float* dvec = nullptr;       // backward workspace: rowsum(dO o O)
-  size_t dvec_elems = 0;
   bool battr_done[8] = {false, false, false, false, false, false, false, false};
   cudaStream_t e2e_stream[3] = {nullptr, nullptr, nullptr};
   cudaEvent_t e2e_ev[2][kE2EChunks + 1] = {};
@@ -325,6 +326,28 @@ int ensure_init(int dev, DevState& st) {
   return ATTN_OK;
 }
 
+// Scheduler counters of a launch on `s` (caller holds st.mu).  The kernels
+// pop their queues with atomics on these counters and the last CTA zeroes
+// them on exit, so two grids may share a slot only if they never run at the
+// same time.  Every stream keeps its own slot (launches on one stream are
+// serialised, so a slot is back at zero when the stream's next grid starts);
+// with more than kCounterSlots streams the least recently used stream's slot
+// is handed over.  Contract (include/attn_numa.h): at most kCounterSlots
+// streams of one device may have attention launches in flight at once.
+unsigned counter_slot(DevState& st, cudaStream_t s) {
+  unsigned best = 0;
+  for (unsigned i = 0; i < kCounterSlots; ++i) {
+    if (st.slot_used[i] != 0 && st.slot_stream[i] == s) {
+      st.slot_used[i] = ++st.slot_tick;
+      return i;
+    }
+    if (st.slot_used[i] < st.slot_used[best]) best = i;
+  }
+  st.slot_stream[best] = s;
+  st.slot_used[best] = ++st.slot_tick;
+  return best;
+}
+
 int current_device(int& dev) {
   ATTN_CUDA(cudaGetDevice(&dev));
   if (dev < 0 || dev >= kMaxDevices) return fail(ATTN_ERR_UNSUPPORTED, "device index beyond kMaxDevices");
@@ -354,9 +377,9 @@ int validate(const void* q, const void* k, const void* v, void* o, int B, int Hq
   if (!q || !k || !v || !o) return fail(ATTN_ERR_INVALID_VALUE, "null pointer");
   if (B <= 0 || Hq <= 0 || Hkv <= 0 || N <= 0 || d <= 0) return fail(ATTN_ERR_INVALID_VALUE, "size <= 0");
   if (Hq % Hkv != 0) return fail(ATTN_ERR_INVALID_VALUE, "Hq % Hkv != 0 (non-uniform GQA groups)");
-  if ((mapping & ~(kMapMask | kOrderDescending | ATTN_CLUSTER_MULTICAST)) || (mapping & kMapMask) > 3)
+  if ((mapping & ~(kMapMask | kOrderDescending | kOrderAlternate | ATTN_CLUSTER_MULTICAST)) || (mapping & kMapMask) > 3)
     return fail(ATTN_ERR_INVALID_VALUE,
-                "mapping not in {0,1,2,3} (| ATTN_ORDER_DESCENDING | ATTN_CLUSTER_MULTICAST)");
+                "mapping not in {0,1,2,3} (| ATTN_ORDER_DESCENDING | ATTN_ORDER_ALTERNATE | ATTN_CLUSTER_MULTICAST)");
   if (!std::isfinite(scale)) return fail(ATTN_ERR_INVALID_VALUE, "non-finite scale");
   const size_t qb = (size_t)B * Hq * N * d * 2, kb = (size_t)B * Hkv * N * d * 2;
   if (overlaps(o, qb, q, qb) || overlaps(o, qb, k, kb) || overlaps(o, qb, v, kb))
@@ -505,6 +528,7 @@ int fwd_impl(const void* q, const void* k, const void* v, void* o, int B, int Hq
     rc = check_dev_ptr(pr.first, dev, pr.second);
     if (rc != ATTN_OK) return rc;
   }
+  if (lse && (rc = check_dev_ptr(lse, dev, "lse")) != ATTN_OK) return rc;
   rc = get_encode();
   if (rc != ATTN_OK) return rc;
   DevState& st = g_dev[dev];
@@ -545,8 +569,7 @@ int fwd_impl(const void* q, const void* k, const void* v, void* o, int B, int Hq
   kp.lse = lse;
   if (!build_sched(mapping, B, Hsched, Hkv, Usched, st.active.n_domains, st.active.sms_per_domain, kp.sched))
     return fail(ATTN_ERR_INVALID_VALUE, "cannot build the schedule");
-  const unsigned slot = st.slot++ % kCounterSlots;
-  kp.counters = st.d_counters + (size_t)slot * kCounterInts;
+  kp.counters = st.d_counters + (size_t)counter_slot(st, stream) * kCounterInts;
   kp.domain_of_smid = st.d_domain;
   kp.n_smid = ATTN_MAX_SMID;
   kp.trace = st.trace;
@@ -623,19 +646,17 @@ int bwd_impl(const void* q, const void* k, const void* v, const void* o, const v
   DevState& st = g_dev[dev];
   std::lock_guard<std::mutex> lk(st.mu);
   if ((rc = ensure_init(dev, st)) != ATTN_OK) return rc;
+  // rowsum(dO o O) workspace, private to this call: allocated and freed in
+  // the order of `stream` (stream-ordered pool), so concurrent backward calls
+  // on other streams never share it.
   const size_t rows = (size_t)B * Hq * N;
-  if (st.dvec_elems < rows) {
-    if (st.dvec) cudaFree(st.dvec);
-    st.dvec = nullptr;
-    st.dvec_elems = 0;
-    ATTN_CUDA(cudaMalloc(&st.dvec, rows * sizeof(float)));
-    st.dvec_elems = rows;
-  }
+  float* dvec = nullptr;
+  ATTN_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dvec), rows * sizeof(float), stream));
   const int nblk = (N + bwd::kBM - 1) / bwd::kBM;
   bwd::BwdParams pq{};
   pq.B = B; pq.Hq = Hq; pq.Hkv = Hkv; pq.N = N; pq.G = Hq / Hkv; pq.nblk = nblk; pq.d_real = d;
   pq.scale = scale; pq.scale_log2 = scale * 1.4426950408889634f;
-  pq.lse = lse; pq.dvec = st.dvec;
+  pq.lse = lse; pq.dvec = dvec;
   pq.dq = reinterpret_cast<__nv_bfloat16*>(dq);
   pq.dk = reinterpret_cast<__nv_bfloat16*>(dk);
   pq.dv = reinterpret_cast<__nv_bfloat16*>(dv);
@@ -647,25 +668,34 @@ int bwd_impl(const void* q, const void* k, const void* v, const void* o, const v
   pq.U = nblk;
   pkv.U = nblk;
   if (!build_sched(mapping, B, Hq, Hkv, nblk, st.active.n_domains, st.active.sms_per_domain, pq.sched) ||
-      !build_sched(mapping, B, Hkv, Hkv, nblk, st.active.n_domains, st.active.sms_per_domain, pkv.sched))
+      !build_sched(mapping, B, Hkv, Hkv, nblk, st.active.n_domains, st.active.sms_per_domain, pkv.sched)) {
+    cudaFreeAsync(dvec, stream);
     return fail(ATTN_ERR_INVALID_VALUE, "cannot build the schedule");
-  pq.counters = st.d_counters + (size_t)(st.slot++ % kCounterSlots) * kCounterInts;
-  pkv.counters = st.d_counters + (size_t)(st.slot++ % kCounterSlots) * kCounterInts;
+  }
+  // the dQ and dK/dV grids run one after the other on `stream`: one slot
+  pq.counters = pkv.counters = st.d_counters + (size_t)counter_slot(st, stream) * kCounterInts;
   CUtensorMap tq, tdo, tk, tv;
-  if ((rc = make_tmap(&tq, q, (long long)B * Hq, N, d, bwd::kBM)) != ATTN_OK) return rc;
-  if ((rc = make_tmap(&tdo, dout, (long long)B * Hq, N, d, bwd::kBM)) != ATTN_OK) return rc;
-  if ((rc = make_tmap(&tk, k, (long long)B * Hkv, N, d, bwd::kBM)) != ATTN_OK) return rc;
-  if ((rc = make_tmap(&tv, v, (long long)B * Hkv, N, d, bwd::kBM)) != ATTN_OK) return rc;
+  if ((rc = make_tmap(&tq, q, (long long)B * Hq, N, d, bwd::kBM)) != ATTN_OK ||
+      (rc = make_tmap(&tdo, dout, (long long)B * Hq, N, d, bwd::kBM)) != ATTN_OK ||
+      (rc = make_tmap(&tk, k, (long long)B * Hkv, N, d, bwd::kBM)) != ATTN_OK ||
+      (rc = make_tmap(&tv, v, (long long)B * Hkv, N, d, bwd::kBM)) != ATTN_OK) {
+    cudaFreeAsync(dvec, stream);
+    return rc;
+  }
   const long long nrows = (long long)rows;
   bwd::attn_bwd_dot_kernel<<<(unsigned)((nrows + 7) / 8), 256, 0, stream>>>(
-      reinterpret_cast<const __nv_bfloat16*>(o), reinterpret_cast<const __nv_bfloat16*>(dout), st.dvec, nrows, d);
-  ATTN_CUDA(cudaGetLastError());
+      reinterpret_cast<const __nv_bfloat16*>(o), reinterpret_cast<const __nv_bfloat16*>(dout), dvec, nrows, d);
+  if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) {
+    cudaFreeAsync(dvec, stream);
+    return cuda_fail(e, "attn_bwd_dot_kernel launch");
+  }
   const int grid_q = std::min(st.num_sms, B * Hq * nblk), grid_kv = std::min(st.num_sms, B * Hkv * nblk);
   const int dpad = d <= 64 ? 64 : 128;
   if (dpad == 128 && causal) rc = launch_bwd_t<128, true>(st, tq, tdo, tk, tv, pq, pkv, grid_q, grid_kv, stream);
   else if (dpad == 128) rc = launch_bwd_t<128, false>(st, tq, tdo, tk, tv, pq, pkv, grid_q, grid_kv, stream);
   else if (causal) rc = launch_bwd_t<64, true>(st, tq, tdo, tk, tv, pq, pkv, grid_q, grid_kv, stream);
   else rc = launch_bwd_t<64, false>(st, tq, tdo, tk, tv, pq, pkv, grid_q, grid_kv, stream);
+  cudaFreeAsync(dvec, stream);  // after the dQ and dK/dV kernels in stream order
   if (rc != ATTN_OK) return rc;
   g_info.kernel_launches = 3;
   g_info.units = B * Hq * nblk + B * Hkv * nblk;
@@ -1024,7 +1054,7 @@ int attn_schedule_order(int B, int Hq, int Hkv, int N, int mapping, int n_domain
     for (int pos = 0; pos < sp.q[qi].len; ++pos) {
       int b, h, u;
       decode_unit(sp.q[qi], pos, Hq, U, b, h, u);
-      if (sp.descending) u = U - 1 - u;
+      if ((sp.descending >> qi) & 1) u = U - 1 - u;
       out[3 * w] = b;
       out[3 * w + 1] = h;
       out[3 * w + 2] = u;
@@ -1066,9 +1096,6 @@ void attn_shutdown(void) {
     cudaSetDevice(dv);
     if (st.d_domain) cudaFree(st.d_domain);
     if (st.d_counters) cudaFree(st.d_counters);
-    if (st.dvec) cudaFree(st.dvec);
-    st.dvec = nullptr;
-    st.dvec_elems = 0;
     for (bool& a : st.battr_done) a = false;
     for (int i = 0; i < 4; ++i)
       if (st.hbuf[i]) cudaFree(st.hbuf[i]);
@@ -1089,6 +1116,7 @@ void attn_shutdown(void) {
     }
     st.init = false;
     for (bool& a : st.attr_done) a = false;
+    for (int i = 0; i < kCounterSlots; ++i) { st.slot_stream[i] = nullptr; st.slot_used[i] = 0; }
   }
 }
 

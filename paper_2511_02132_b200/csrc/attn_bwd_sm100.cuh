@@ -116,7 +116,7 @@ __device__ __forceinline__ void bwd_scheduler(const BwdParams& p, BCtrl* ctrl, i
       const int pos = atomicAdd(&p.counters[qq * 32], 1);
       if (pos < p.sched.q[qq].len) {
         decode_unit(p.sched.q[qq], pos, Hsched, p.U, b, h, u);
-        if (p.sched.descending) u = p.U - 1 - u;
+        if ((p.sched.descending >> qq) & 1) u = p.U - 1 - u;
         qi = qq;
         break;
       }

@@ -46,7 +46,7 @@ struct QueueDesc {
 struct SchedParams {
   int n_queues;
   int steal;                           // pop other queues when the own one is empty
-  int descending;                      // units of a head in descending order (longest causal unit first)
+  int descending;                      // bit q set: queue q visits each head's units in descending order
   int queue_of_domain[kMaxQueues];     // die -> queue popped first
   QueueDesc q[kMaxQueues];
 };
@@ -90,17 +90,27 @@ inline int prop_cut(long long total, const int* sizes, int n, int d) {
 
 // Mapping argument: low byte = mapping (0 BF, 1 HF, 2 SHF, 3 SBF); bit 8 =
 // descending unit order inside every (b, h) (applied identically to every
-// mapping; the paper's order is ascending).
+// mapping; the paper's order is ascending); bit 10 = alternate the unit
+// direction per queue (queue d descending iff d is odd; single-queue
+// mappings are unaffected) -- see include/attn_numa.h ATTN_ORDER_ALTERNATE.
 constexpr int kMapMask = 0xff;
 constexpr int kOrderDescending = 0x100;
+constexpr int kOrderAlternate = 0x400;
+
+// Per-queue direction mask of an order argument for n_queues queues.
+ATTN_HD int direction_mask(int mapping_arg, int n_queues) {
+  const int all = (1 << n_queues) - 1;
+  int m = (mapping_arg & kOrderDescending) ? all : 0;
+  if (mapping_arg & kOrderAlternate) m ^= (0xAA & all);
+  return m;
+}
 
 // Build the queues of `mapping` for n_domains dies.  Returns false on bad arguments.
-inline bool build_sched(int mapping_arg, int B, int Hq, int Hkv, int U, int n_domains, const int* sms_per_domain,
-                        SchedParams& sp) {
+inline bool build_queues(int mapping_arg, int B, int Hq, int Hkv, int U, int n_domains, const int* sms_per_domain,
+                         SchedParams& sp) {
   sp = SchedParams{};
-  if (mapping_arg & ~(kMapMask | kOrderDescending)) return false;
+  if (mapping_arg & ~(kMapMask | kOrderDescending | kOrderAlternate)) return false;
   const int mapping = mapping_arg & kMapMask;
-  sp.descending = (mapping_arg & kOrderDescending) ? 1 : 0;
   if (B <= 0 || Hq <= 0 || Hkv <= 0 || U <= 0 || Hq % Hkv != 0) return false;
   if (n_domains < 1 || n_domains > kMaxQueues) return false;
   const int G = Hq / Hkv;
@@ -141,6 +151,13 @@ inline bool build_sched(int mapping_arg, int B, int Hq, int Hkv, int U, int n_do
       sp.q[d] = QueueDesc{1, t0, t1 - t0, 0, Hq, 0, 0};
     }
   }
+  return true;
+}
+
+inline bool build_sched(int mapping_arg, int B, int Hq, int Hkv, int U, int n_domains, const int* sms_per_domain,
+                        SchedParams& sp) {
+  if (!build_queues(mapping_arg, B, Hq, Hkv, U, n_domains, sms_per_domain, sp)) return false;
+  sp.descending = direction_mask(mapping_arg, sp.n_queues);
   return true;
 }
 

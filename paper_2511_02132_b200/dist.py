@@ -58,29 +58,41 @@ def env_rank_world():
         int(os.environ.get("LOCAL_RANK", "0"))
 
 
-def init(backend: Optional[str] = None) -> tuple:
+def init(backend: Optional[str] = None, nccl_debug_init: bool = False, force: bool = False) -> tuple:
     """Initialise the default process group from torchrun's env (127.0.0.1 rendezvous).
 
-    ATTN_BENCH_SHARE_GPU=1 (tests only): every rank uses cuda:0 and gloo, so
-    the multi-rank code path can be exercised on a one-GPU box."""
+    Only for world > 1, or with force=True under torchrun (a process group of
+    one rank, so the NCCL collective path itself can be exercised on one GPU).
+    nccl_debug_init: NCCL_DEBUG=INFO scoped to the INIT subsystem unless the
+    caller set NCCL_DEBUG, so communicator creation (ranks, transports, NVLS)
+    is visible in the log.  ATTN_BENCH_SHARE_GPU=1 (tests only): every rank
+    uses cuda:0 and gloo, so the multi-rank code path runs on a one-GPU box."""
     rank, world, local = env_rank_world()
     if os.environ.get("ATTN_BENCH_SHARE_GPU") == "1":
         local = 0
         backend = "gloo"
-    if world > 1 and not dist.is_initialized():
+    under_torchrun = "RANK" in os.environ and "MASTER_PORT" in os.environ
+    if (world > 1 or (force and under_torchrun)) and not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         if backend is None:
             backend = "nccl" if torch.cuda.is_available() else "gloo"
         if backend == "nccl":
+            if nccl_debug_init and "NCCL_DEBUG" not in os.environ:
+                os.environ["NCCL_DEBUG"] = "INFO"
+                os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             torch.cuda.set_device(local)
-        dist.init_process_group(backend=backend)
+            dist.init_process_group(backend=backend, device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend=backend)
     return rank, world, local
 
 
 def all_gather_heads(o_local: torch.Tensor, world: int, group=None) -> torch.Tensor:
     """Replicated O from per-rank head shards [B, Hq/G, N, d] -> [B, Hq, N, d]."""
     B, hq, N, d = o_local.shape
-    if world == 1:
+    if not (dist.is_available() and dist.is_initialized()):
+        if world != 1:
+            raise RuntimeError("all_gather_heads: no process group for world > 1")
         return o_local
     buf = torch.empty((world, B, hq, N, d), dtype=o_local.dtype, device=o_local.device)
     if dist.get_backend(group) == "nccl":
@@ -147,7 +159,9 @@ def replicated_fwd(q, k, v, shard: HeadShard, out: PeerOutput, *, causal: bool =
     Hq_out = out.local.shape[1]
     api.attn_fwd_replicated(q, k, v, dsts, Hq_out, shard.q_lo, causal=causal, scale=scale, mapping=mapping, **kw)
     if sync:
-        torch.cuda.current_stream().synchronize()
+        # the stream the epilogue's peer stores were enqueued on, not merely
+        # the current one: the barrier below must not pass before they land
+        (kw.get("stream") or torch.cuda.current_stream()).synchronize()
         if out.world > 1:
             dist.barrier(group=out.group)
     return out.local

@@ -23,22 +23,25 @@ def slice_seed(base: int, tensor: str, b: int, head: int) -> int:
 
 
 def make_tensor(tensor: str, B: int, H: int, N: int, d: int, *, base: int = 0,
-                head_offset: int = 0, device="cpu", dtype=torch.bfloat16) -> torch.Tensor:
-    """[B, H, N, d] tensor whose (b, h) slice is drawn from slice_seed(.., b, head_offset + h)."""
+                head_offset: int = 0, batch_offset: int = 0, device="cpu", dtype=torch.bfloat16) -> torch.Tensor:
+    """[B, H, N, d] tensor whose (b, h) slice is drawn from
+    slice_seed(.., batch_offset + b, head_offset + h): any sub-block of heads
+    and batch items is bit-identical to that slice of the full tensor."""
     out = torch.empty((B, H, N, d), dtype=dtype, device=device)
     gen = torch.Generator(device=device)
     for b in range(B):
         for h in range(H):
-            gen.manual_seed(slice_seed(base, tensor, b, head_offset + h))
+            gen.manual_seed(slice_seed(base, tensor, batch_offset + b, head_offset + h))
             x = torch.randn((N, d), generator=gen, device=device, dtype=torch.float32)
             out[b, h].copy_(x.to(dtype))
     return out
 
 
 def make_qkv(B: int, Hq: int, Hkv: int, N: int, d: int, *, base: int = 0,
-             q_head_offset: int = 0, kv_head_offset: int = 0, device="cpu",
+             q_head_offset: int = 0, kv_head_offset: int = 0, batch_offset: int = 0, device="cpu",
              dtype=torch.bfloat16):
-    q = make_tensor("q", B, Hq, N, d, base=base, head_offset=q_head_offset, device=device, dtype=dtype)
-    k = make_tensor("k", B, Hkv, N, d, base=base, head_offset=kv_head_offset, device=device, dtype=dtype)
-    v = make_tensor("v", B, Hkv, N, d, base=base, head_offset=kv_head_offset, device=device, dtype=dtype)
+    kw = dict(base=base, batch_offset=batch_offset, device=device, dtype=dtype)
+    q = make_tensor("q", B, Hq, N, d, head_offset=q_head_offset, **kw)
+    k = make_tensor("k", B, Hkv, N, d, head_offset=kv_head_offset, **kw)
+    v = make_tensor("v", B, Hkv, N, d, head_offset=kv_head_offset, **kw)
     return q, k, v

@@ -48,7 +48,7 @@ def _fwd(lib, q=1 << 20, k=2 << 20, v=3 << 20, o=4 << 20, B=1, Hq=2, Hkv=2, N=12
 
 @pytest.mark.parametrize("kw,status", [
     (dict(q=0), 1), (dict(o=0), 1), (dict(B=0), 1), (dict(N=-1), 1), (dict(Hq=6, Hkv=4), 1),
-    (dict(mapping=4), 1), (dict(mapping=-1), 1), (dict(mapping=0x400), 1), (dict(mapping=0x204), 1), (dict(mapping=0x104), 1), (dict(scale=float("nan")), 1), (dict(scale=float("inf")), 1),
+    (dict(mapping=4), 1), (dict(mapping=-1), 1), (dict(mapping=0x800), 1), (dict(mapping=0x404), 1), (dict(mapping=0x204), 1), (dict(mapping=0x104), 1), (dict(scale=float("nan")), 1), (dict(scale=float("inf")), 1),
     (dict(d=100), 2), (dict(d=136), 2), (dict(scale=-0.5), 2), (dict(q=(1 << 20) + 8), 2),
     (dict(o=(1 << 20) + 64), 1),   # o overlaps q
 ])
@@ -95,6 +95,19 @@ def test_schedule_order_descending_matches_oracle(lib):
         for m in om.MAPPINGS:
             got = api.attn_schedule_order(B, Hq, Hkv, N, m, [74, 74], order="descending")
             assert got == om.descending(om.build_queues(m, B, Hq, Hkv, U, [74, 74]), U)
+
+
+def test_schedule_order_alternate_matches_oracle(lib):
+    rng = random.Random(17)
+    for _ in range(30):
+        Hkv = rng.choice([1, 2, 3, 4, 8])
+        Hq = Hkv * rng.choice([1, 2])
+        B, N = rng.randint(1, 2), 128 * rng.randint(1, 10)
+        U = (N + 255) // 256
+        sizes = [rng.randint(60, 80) for _ in range(rng.randint(1, 3))]
+        for m in om.MAPPINGS:
+            got = api.attn_schedule_order(B, Hq, Hkv, N, m, sizes, order="alternate")
+            assert got == om.alternate(om.build_queues(m, B, Hq, Hkv, U, sizes), U)
 
 
 def test_schedule_order_cluster_units_match_oracle(lib):

@@ -27,7 +27,7 @@ def test_bench_two_ranks_share_gpu(workload, scaling):
     steps = "3" if workload == "C2" else "1"
     out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                           "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "2",
-                          "--steps", steps, "--warmup", "3", "--workload", workload],
+                          "--steps", steps, "--warmup", "3", "--workload", workload, "--ncu", "off"],
                          cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
     assert out.returncode == 0, out.stderr[-3000:]
     lines = [l for l in out.stdout.splitlines() if l.startswith("{")]

@@ -109,6 +109,26 @@ def test_full_size_sampled_rows(name, B, Hq, Hkv, N, d, causal):
     assert torch.equal(o.view(torch.int16), o2.view(torch.int16))
 
 
+def test_c2_full_tensor_parity():
+    """BASELINE config 2 in FULL (SURVEY.md §8(c): full tensors for C1 and C2;
+    C1's shape is the first SMALL case): all 32 x 8192 rows x 128 columns of
+    the fp64 oracle (eq:fa; ~1.1e12 fp64 flop on the host's
+    threads) against the launch configuration bench.py times (SHF, CTA-pair
+    clusters), and the plain SHF launch bit for bit."""
+    import os
+
+    B, Hq, Hkv, N, d = 1, 32, 32, 8192, 128
+    q, k, v = synth.make_qkv(B, Hq, Hkv, N, d, base=2, device="cuda")
+    o = torch.full_like(q, float("nan"))
+    attn_fwd(q, k, v, o, causal=False, mapping="swizzled_head_first", cluster=True)
+    o_plain = _run(q, k, v, False, "swizzled_head_first")
+    oa.set_threads(len(os.sched_getaffinity(0)))
+    ref = oa.attention(q.cpu(), k.cpu(), v.cpu(), causal=False, scale=1.0 / math.sqrt(d))
+    err = _check(o, ref, "C2 full tensor")
+    assert err.size == B * Hq * N * d
+    assert torch.equal(o.view(torch.int16), o_plain.view(torch.int16))
+
+
 def test_causal_row0_is_v0_bitexact():
     q, k, v = synth.make_qkv(1, 4, 4, 512, 128, base=3, device="cuda")
     o = _run(q, k, v, True, "swizzled_head_first")

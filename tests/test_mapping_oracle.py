@@ -178,3 +178,32 @@ def test_single_domain_degenerates_to_head_first():
     for B, Hq, Hkv, nblk in ((1, 4, 4, 3), (2, 8, 2, 5)):
         assert (om.build_queues("swizzled_head_first", B, Hq, Hkv, nblk, [148])
                 == om.build_queues("head_first", B, Hq, Hkv, nblk, [148]))
+
+
+def test_descending_worked_example():
+    """DESIGN.md R19 written out by hand (not recomputed): Z=1, Hq=Hkv=4, three
+    query blocks, two equal dies.  Descending visits each head's blocks
+    last-first and changes nothing else -- same queues, same heads per die."""
+    shf = om.build_queues(om.SWIZZLED_HEAD_FIRST, 1, 4, 4, 3, [74, 74])
+    assert om.descending(shf, 3) == [
+        [(0, 0, 2), (0, 0, 1), (0, 0, 0), (0, 1, 2), (0, 1, 1), (0, 1, 0)],
+        [(0, 2, 2), (0, 2, 1), (0, 2, 0), (0, 3, 2), (0, 3, 1), (0, 3, 0)],
+    ]
+    bf = om.build_queues(om.BLOCK_FIRST, 1, 2, 2, 3, [74, 74])
+    assert om.descending(bf, 3) == [[(0, 0, 2), (0, 1, 2), (0, 0, 1), (0, 1, 1), (0, 0, 0), (0, 1, 0)]]
+    # GQA (Hq=4, Hkv=2), two batch items, two blocks: die 1 keeps group 1 (heads 2, 3) of every batch item
+    g = om.build_queues(om.SWIZZLED_HEAD_FIRST, 2, 4, 2, 2, [74, 74])
+    assert om.descending(g, 2)[1] == [(0, 2, 1), (0, 2, 0), (0, 3, 1), (0, 3, 0),
+                                      (1, 2, 1), (1, 2, 0), (1, 3, 1), (1, 3, 0)]
+
+
+def test_alternate_worked_example():
+    """DESIGN.md R22 by hand: queue 0 ascending, queue 1 descending; a single
+    queue (head-first) is unchanged."""
+    shf = om.build_queues(om.SWIZZLED_HEAD_FIRST, 1, 4, 4, 3, [74, 74])
+    assert om.alternate(shf, 3) == [
+        [(0, 0, 0), (0, 0, 1), (0, 0, 2), (0, 1, 0), (0, 1, 1), (0, 1, 2)],
+        [(0, 2, 2), (0, 2, 1), (0, 2, 0), (0, 3, 2), (0, 3, 1), (0, 3, 0)],
+    ]
+    hf = om.build_queues(om.HEAD_FIRST, 1, 2, 2, 2, [74, 74])
+    assert om.alternate(hf, 2) == [[(0, 0, 0), (0, 0, 1), (0, 1, 0), (0, 1, 1)]]
