@@ -134,10 +134,14 @@ typedef struct {
   signed char domain_of_smid[ATTN_MAX_SMID];/* -1 for ids never observed */
   float lat_near_cyc;                       /* median L2-hit latency, near lines */
   float lat_far_cyc;                        /* median L2-hit latency, far lines */
-  int far_lines_cached_near;                /* 1 if repeated far reads became near */
+  int far_lines_cached_near;                /* measured: 1 if a far line re-read after its first
+                                               (ld.global.cg) access comes back at the near
+                                               latency, i.e. the reading die keeps a copy */
   long long l2_bytes;                       /* cudaDevAttrL2CacheSize */
   int source;                               /* 0 probe, 1 override, 2 fallback (1 domain) */
   int stable;                               /* 1 if two probe runs agreed */
+  float lat_near_reread_cyc;                /* median re-read latency of near lines after a flush */
+  float lat_far_reread_cyc;                 /* same for far lines (probe SM of each die) */
 } attn_topology_t;
 
 /* One record per work unit when a schedule trace buffer is installed. */

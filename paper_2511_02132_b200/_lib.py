@@ -36,6 +36,8 @@ class Topology(ctypes.Structure):
         ("l2_bytes", ctypes.c_longlong),
         ("source", ctypes.c_int),
         ("stable", ctypes.c_int),
+        ("lat_near_reread_cyc", ctypes.c_float),
+        ("lat_far_reread_cyc", ctypes.c_float),
     ]
 
 

@@ -246,6 +246,7 @@ def attn_topology(device: int = 0) -> Dict:
         "domain_of_smid": list(t.domain_of_smid)[: t.nsmid],
         "lat_near_cyc": t.lat_near_cyc, "lat_far_cyc": t.lat_far_cyc,
         "far_lines_cached_near": t.far_lines_cached_near, "l2_bytes": t.l2_bytes,
+        "lat_near_reread_cyc": t.lat_near_reread_cyc, "lat_far_reread_cyc": t.lat_far_reread_cyc,
         "source": ("probe", "override", "fallback")[t.source] if 0 <= t.source <= 2 else t.source,
         "stable": bool(t.stable),
     }

@@ -198,6 +198,62 @@ bool classify(const std::vector<uint32_t>& lat, const std::vector<int>& present,
   return true;
 }
 
+// SURVEY.md §8(a1) step 6, measured: for one SM of each die, flush L2, touch
+// every probe line once and time its re-reads (topo_reread_kernel).  Which
+// lines are far for an SM comes from the latency matrix: per line, the die
+// whose SMs see the higher mean latency is the far one.  far_lines_cached_near
+// = 1 if far lines re-read closer to the near than to the far latency.
+int measure_reread(attn_topology_t& t, const std::vector<int>& present, const std::vector<uint32_t>& lat,
+                   const uint32_t* d_probe) {
+  const int L = kProbeLines;
+  std::vector<double> mean[2] = {std::vector<double>(L, 0.0), std::vector<double>(L, 0.0)};
+  int cnt[2] = {0, 0};
+  for (int s : present) {
+    const int dm = t.domain_of_smid[s];
+    for (int l = 0; l < L; ++l) mean[dm][l] += lat[(size_t)s * L + l];
+    ++cnt[dm];
+  }
+  if (cnt[0] == 0 || cnt[1] == 0) return ATTN_OK;
+  for (int dm = 0; dm < 2; ++dm)
+    for (int l = 0; l < L; ++l) mean[dm][l] /= cnt[dm];
+  size_t l2 = (size_t)t.l2_bytes;
+  void* flush = nullptr;
+  int *d_claimed = nullptr;
+  uint32_t* d_rr = nullptr;
+  ATTN_CUDA(cudaMalloc(&flush, 2 * l2));
+  ATTN_CUDA(cudaMalloc(&d_claimed, sizeof(int)));
+  ATTN_CUDA(cudaMalloc(&d_rr, sizeof(uint32_t) * L));
+  std::vector<double> near_rr, far_rr;
+  for (int dm = 0; dm < 2; ++dm) {
+    int target = -1;
+    for (int s : present)
+      if (t.domain_of_smid[s] == dm) { target = s; break; }
+    ATTN_CUDA(cudaMemset(flush, dm + 1, 2 * l2));  // evict the probe lines from L2
+    ATTN_CUDA(cudaMemset(d_claimed, 0, sizeof(int)));
+    ATTN_CUDA(cudaMemset(d_rr, 0xFF, sizeof(uint32_t) * L));
+    topo_reread_kernel<<<8 * t.num_sms, 32>>>(d_probe, d_claimed, target, d_rr);
+    ATTN_CUDA(cudaGetLastError());
+    ATTN_CUDA(cudaDeviceSynchronize());
+    std::vector<uint32_t> rr(L);
+    ATTN_CUDA(cudaMemcpy(rr.data(), d_rr, sizeof(uint32_t) * L, cudaMemcpyDeviceToHost));
+    for (int l = 0; l < L; ++l) {
+      if (rr[l] == 0xFFFFFFFFu) continue;  // target SM never ran a CTA (cannot happen with 8 CTAs per SM)
+      (mean[dm][l] > mean[1 - dm][l] ? far_rr : near_rr).push_back(rr[l]);
+    }
+  }
+  cudaFree(flush);
+  cudaFree(d_claimed);
+  cudaFree(d_rr);
+  if (near_rr.empty() || far_rr.empty()) return ATTN_OK;
+  std::sort(near_rr.begin(), near_rr.end());
+  std::sort(far_rr.begin(), far_rr.end());
+  t.lat_near_reread_cyc = (float)near_rr[near_rr.size() / 2];
+  t.lat_far_reread_cyc = (float)far_rr[far_rr.size() / 2];
+  t.far_lines_cached_near =
+      (t.lat_far_reread_cyc - t.lat_near_reread_cyc) < 0.5f * (t.lat_far_cyc - t.lat_near_cyc) ? 1 : 0;
+  return ATTN_OK;
+}
+
 int run_probe(int dev, DevState& st) {
   attn_topology_t t{};
   memset(t.domain_of_smid, -1, sizeof(t.domain_of_smid));
@@ -249,8 +305,10 @@ int run_probe(int dev, DevState& st) {
   std::vector<uint32_t> lat_a, lat_b;
   int rc = probe_once(nsmid, d_probe, lat_a, t.num_sms);
   if (rc == ATTN_OK) rc = probe_once(nsmid, d_probe, lat_b, t.num_sms);
-  cudaFree(d_probe);
-  if (rc != ATTN_OK) return rc;
+  if (rc != ATTN_OK) {
+    cudaFree(d_probe);
+    return rc;
+  }
   if (const char* dump = getenv("ATTN_NUMA_PROBE_DUMP")) {
     if (FILE* f = fopen(dump, "w")) {
       for (int s : present) {
@@ -283,6 +341,7 @@ int run_probe(int dev, DevState& st) {
   t.lat_far_cyc = fa;
   t.stable = same ? 1 : 0;
   if (!same) {
+    cudaFree(d_probe);
     fallback_topology(t);
     st.measured = t;
     return ATTN_OK;
@@ -293,9 +352,9 @@ int run_probe(int dev, DevState& st) {
     t.domain_of_smid[s] = dom_a[s];
     ++t.sms_per_domain[(int)dom_a[s]];
   }
-  // Far lines stayed far across rounds (min over rounds), so a far line is
-  // not replicated into the near L2 by repeated .cg reads.
-  t.far_lines_cached_near = 0;
+  rc = measure_reread(t, present, lat_a, d_probe);
+  cudaFree(d_probe);
+  if (rc != ATTN_OK) return rc;
   t.source = 0;
   st.measured = t;
   return ATTN_OK;
@@ -396,18 +455,6 @@ int validate(const void* q, const void* k, const void* v, void* o, int B, int Hq
 // 3-D view [heads][N][d] of a [B][H][N][d] tensor: a box never crosses into
 // the next head, and rows >= N are out of bounds (zero-filled by TMA).
 int make_tmap(CUtensorMap* m, const void* base, long long heads, int N, int d, int box_rows) {
-#ifdef ATTN_TMA_2D
-  {
-    cuuint64_t dims2[2] = {(cuuint64_t)d, (cuuint64_t)N * heads};
-    cuuint64_t strides2[1] = {(cuuint64_t)d * 2};
-    cuuint32_t box2[2] = {64, (cuuint32_t)box_rows};
-    cuuint32_t estr2[2] = {1, 1};
-    CUresult r2 = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims2, strides2, box2,
-                           estr2, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r2 == CUDA_SUCCESS ? ATTN_OK : fail(ATTN_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-  }
-#endif
   cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)N, (cuuint64_t)heads};
   cuuint64_t strides[2] = {(cuuint64_t)d * 2, (cuuint64_t)N * d * 2};
   cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};

@@ -31,6 +31,7 @@
 
 #include "../../include/attn_numa.h"
 #include "attn_sched.h"
+#include "instrument.cuh"
 #include "ptx.cuh"
 
 namespace attn {
@@ -286,8 +287,7 @@ __device__ __forceinline__ void run_scheduler(const KernelParams& p, CT* ctrl) {
       ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&ctrl->sched_full[stage]), 1));
     }
     if (qi < 0) break;
-#if !defined(ATTN_PROFILE_WAITS) && !defined(ATTN_TIMELINE) && !defined(ATTN_CYCLES)
-    if (kCl == 1 && p.trace) {
+    if (kCl == 1 && p.trace && !ATTN_INSTRUMENTED) {  // instrumented builds reuse p.trace
       const long long id = ((long long)b * p.Hq + h) * p.U + u;
       if (id < p.trace_cap) {
         attn_trace_rec_t r;
@@ -296,7 +296,6 @@ __device__ __forceinline__ void run_scheduler(const KernelParams& p, CT* ctrl) {
         p.trace[id] = r;
       }
     }
-#endif
     ++seq;
     if (++stage == kSchedRing) { stage = 0; phase ^= 1; }
   }
@@ -426,13 +425,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int bh = b * p.Hq + h, row = (2 * u + t) * kBlockM;
 #pragma unroll
           for (int c = 0; c < C::kChunks; ++c)
-#ifdef ATTN_TMA_2D
-            ptx::tma_load_2d(q_smem + t * C::kQTileBytes + c * kBlockM * 128, &tm_q, &ctrl->q_full, c * 64,
-                             bh * p.N + row, pol_q);
-#else
             ptx::tma_load_3d(q_smem + t * C::kQTileBytes + c * kBlockM * 128, &tm_q, &ctrl->q_full, c * 64, row, bh,
                              pol_q);
-#endif
         }
         }
         const int kvbh = b * p.Hkv + h / p.G;
@@ -463,24 +457,12 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (++kv_stage == C::kStages) { kv_stage = 0; kv_phase ^= 1; }
               continue;
             }
-#ifdef ATTN_DEBUG_NO_KV_LOAD
-            if (j >= 2) {  // bandwidth probe: reuse whatever is in the slot
-              ptx::mbar_arrive(&ctrl->kv_full[kv_stage]);
-              if (++kv_stage == C::kStages) { kv_stage = 0; kv_phase ^= 1; }
-              continue;
-            }
-#endif
             ptx::mbar_arrive_expect_tx(&ctrl->kv_full[kv_stage], C::kKVBytes);
             uint8_t* dst = kv_smem + kv_stage * C::kKVBytes;
 #pragma unroll
             for (int c = 0; c < C::kChunks; ++c)
-#ifdef ATTN_TMA_2D
-              ptx::tma_load_2d(dst + c * kBlockN * 128, which == 0 ? (const void*)&tm_k : (const void*)&tm_v,
-                               &ctrl->kv_full[kv_stage], c * 64, kvbh * p.N + j * kBlockN, pol_kv);
-#else
               ptx::tma_load_3d(dst + c * kBlockN * 128, which == 0 ? (const void*)&tm_k : (const void*)&tm_v,
                                &ctrl->kv_full[kv_stage], c * 64, j * kBlockN, kvbh, pol_kv);
-#endif
             if (++kv_stage == C::kStages) { kv_stage = 0; kv_phase ^= 1; }
           }
         }
@@ -502,11 +484,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(&ctrl->tmem_base);
     SchedReader<kCl> sr;
     constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(kBlockM, kBlockN, 0, 0);
-#ifdef ATTN_DEBUG_PV_KMAJOR
-    constexpr uint32_t idesc_o = ptx::idesc_bf16_f32(kBlockM, D, 0, 0);  // wrong layout: speed probe only
-#else
     constexpr uint32_t idesc_o = ptx::idesc_bf16_f32(kBlockM, D, 0, 1);
-#endif
     // descriptors at k = 0; advancing K by 16 elements adds 32 B (2 in the
     // >>4 address field) inside a 128-byte swizzle atom, and one atom
     // (rows * 128 B) every 4 steps.
@@ -514,7 +492,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t dkv0 = ptx::smem_desc_sw128(ptx::smem_u32(kv_smem), 16, 1024);
     const uint64_t dv0 = ptx::smem_desc_sw128(ptx::smem_u32(kv_smem), kBlockN * 128, 1024);
     uint32_t q_phase = 0, p_phase0 = 0, p_phase1 = 0;
-    [[maybe_unused]] int unit_no = -1;
     [[maybe_unused]] int extra_blocks = 0;
     int kv_stage = 0;
     uint32_t kv_phase = 0;
@@ -525,14 +502,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t dq = dq0 + (uint64_t)((t * C::kQTileBytes) >> 4);
       const uint64_t dk = dkv0 + (uint64_t)((slot * C::kKVBytes) >> 4);
       const uint32_t d_tmem = tmem + C::col_s(t);
-#ifndef ATTN_DEBUG_NO_S
 #pragma unroll
       for (int k = 0; k < D / 16; ++k) {
         const uint32_t oq = ((k >> 2) * (kBlockM * 128) + (k & 3) * 32) >> 4;
         const uint32_t ok = ((k >> 2) * (kBlockN * 128) + (k & 3) * 32) >> 4;
         ptx::mma_ss(d_tmem, dq + oq, dk + ok, idesc_s, k > 0 ? 1u : 0u);
       }
-#endif
     };
     // O_t += P_t V: K = 128 keys in 8 steps of 16; the steps of slice h read
     // the part of P the softmax publishes separately (p_ready[t][h]).
@@ -540,23 +515,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t dv = dv0 + (uint64_t)((slot * C::kKVBytes) >> 4);
       const uint32_t d_tmem = tmem + C::col_o(t);
       const uint32_t a_tmem = tmem + (kSepP ? C::col_p(t) : C::col_s(t));
-#ifndef ATTN_DEBUG_NO_PV
 #pragma unroll
       for (int k = h * (8 / kPParts); k < (h + 1) * (8 / kPParts); ++k)
         ptx::mma_ts(d_tmem, a_tmem + k * 8, dv + (uint64_t)((k * 16 * 128) >> 4), idesc_o,
                     (acc || k > 0) ? 1u : 0u);
-#endif
     };
-#ifdef ATTN_PROFILE_WAITS
-    long long w_q = 0, w_kv = 0, w_p0 = 0, w_p1 = 0, w_sched = 0;
-    const long long t_start = clock64();
-#define ATTN_TIMED(acc, stmt) { const long long t0_ = clock64(); stmt; acc += clock64() - t0_; }
-#else
-#define ATTN_TIMED(acc, stmt) stmt;
-#endif
     auto take_slot = [&]() {
       const int s = kv_stage;
-      ATTN_TIMED(w_kv, ptx::mbar_wait(&ctrl->kv_full[s], kv_phase));
+      ptx::mbar_wait(&ctrl->kv_full[s], kv_phase);
       if (++kv_stage == C::kStages) { kv_stage = 0; kv_phase ^= 1; }
       return s;
     };
@@ -568,8 +534,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
 
     while (true) {
-      int4 e;
-      ATTN_TIMED(w_sched, e = sr.next(ctrl, false));
+      const int4 e = sr.next(ctrl, false);
       __syncwarp();
       if (lane == 0) sr.release_prev(ctrl);
       if (!e.w) break;
@@ -595,13 +560,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // Separate-P order: S_t(j+1) as soon as the softmax has S_t(j) in
         // registers (s_free), PV_t(j) when P_t(j) is published; p_free / o_ready
         // tell the softmax when P_t may be overwritten and O_t rescaled / read.
-        ATTN_TIMED(w_q, ptx::mbar_wait(&ctrl->q_full, q_phase));
-        ++unit_no;
+        ptx::mbar_wait(&ctrl->q_full, q_phase);
         q_phase ^= 1;
-#ifdef ATTN_TIMELINE
-        long long* tlm = (p.trace && blockIdx.x == 0 && unit_no == 0) ? reinterpret_cast<long long*>(p.trace) + 2048 : nullptr;
-        int jst = -1;  // block index for the stamps inside issue_s_sep
-#endif
         auto issue_s_sep = [&](int t, int slot) {
           int& used = (t == 0) ? s_used0 : s_used1;
           uint32_t& sfp = (t == 0) ? sf_phase0 : sf_phase1;
@@ -609,9 +569,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_wait(&ctrl->s_free[t], sfp);
             sfp ^= 1;
           }
-#ifdef ATTN_TIMELINE
-          if (tlm && lane == 0 && jst >= 0 && jst < 64) tlm[512 + jst * 2 + t] = clock64();
-#endif
           used = 1;
           ptx::tc_fence_after();
           if (ptx::elect_one_sync()) {
@@ -628,20 +585,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (n == 1) ptx::mma_commit(&ctrl->q_empty);
         }
         __syncwarp();
-#ifdef ATTN_TIMELINE
-#define ATTN_MSTAMP(i) if (tlm && lane == 0 && j < 64) tlm[j * 8 + (i)] = clock64(); jst = j;
-#else
-#define ATTN_MSTAMP(i)
-#endif
         for (int j = 0; j < n; ++j) {
-          ATTN_MSTAMP(0);
           if (j + 1 < n) {
             sK = take_slot();
-            ATTN_MSTAMP(1);
             if (j + 1 < n0) issue_s_sep(0, sK);
-            ATTN_MSTAMP(2);
             if (j + 1 < n1) issue_s_sep(1, sK);
-            ATTN_MSTAMP(3);
             if (ptx::elect_one_sync()) {
               kv_release(sK);
               if (j + 2 == n) ptx::mma_commit(&ctrl->q_empty);
@@ -656,9 +604,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint32_t ph = (t == 0) ? p_phase0 : p_phase1;
 #pragma unroll
               for (int h = 0; h < kPParts; ++h) {
-                if (t == 0) { ATTN_TIMED(w_p0, ptx::mbar_wait(&ctrl->p_ready[t][h], ph)); }
-                else { ATTN_TIMED(w_p1, ptx::mbar_wait(&ctrl->p_ready[t][h], ph)); }
-                if (h == 1) { ATTN_MSTAMP(6 + t); }
+                ptx::mbar_wait(&ctrl->p_ready[t][h], ph);
                 ptx::tc_fence_after();
                 if (ptx::elect_one_sync()) issue_pv_half(t, sV, j > 0, h);
                 __syncwarp();
@@ -666,7 +612,6 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (t == 0) p_phase0 ^= 1; else p_phase1 ^= 1;
               if (ptx::elect_one_sync()) ptx::mma_commit(j + 1 < nt ? &ctrl->p_free[t] : &ctrl->o_ready[t]);
               __syncwarp();
-              ATTN_MSTAMP(4 + t);
             }
           }
           if (ptx::elect_one_sync()) kv_release(sV);
@@ -674,8 +619,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         continue;
       }
-      ATTN_TIMED(w_q, ptx::mbar_wait(&ctrl->q_full, q_phase));
-      ++unit_no;
+      ptx::mbar_wait(&ctrl->q_full, q_phase);
       q_phase ^= 1;
       int sK = take_slot();
       ptx::tc_fence_after();
@@ -692,19 +636,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (n == 1) ptx::mma_commit(&ctrl->q_empty);
       }
       __syncwarp();
-#ifdef ATTN_TIMELINE
-      long long* tl = (p.trace && blockIdx.x == 0) ? reinterpret_cast<long long*>(p.trace) : nullptr;
-      if (tl && lane == 0) tl[1000] = clock64();
-#define ATTN_STAMP(i) if (tl && lane == 0 && j < 64 && unit_no == 0) tl[j * 8 + (i)] = clock64();
-#else
-#define ATTN_STAMP(i)
-#endif
       for (int j = 0; j < n; ++j) {
-        ATTN_STAMP(0);
         const int sV = take_slot();
         const bool nxt = j + 1 < n;
         if (nxt) sK = take_slot();
-        ATTN_STAMP(1);
         ptx::tc_fence_after();
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
@@ -713,9 +648,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t ph = (t == 0) ? p_phase0 : p_phase1;
 #pragma unroll
             for (int h = 0; h < kPParts; ++h) {
-              if (t == 0) { ATTN_TIMED(w_p0, ptx::mbar_wait(&ctrl->p_ready[t][h], ph)); }
-              else { ATTN_TIMED(w_p1, ptx::mbar_wait(&ctrl->p_ready[t][h], ph)); }
-              if (h == kPParts - 1) { ATTN_STAMP(2 + 2 * t); }
+              ptx::mbar_wait(&ctrl->p_ready[t][h], ph);
               ptx::tc_fence_after();
               if (ptx::elect_one_sync()) issue_pv_half(t, sV, j > 0, h);
               __syncwarp();
@@ -730,7 +663,6 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
             __syncwarp();
-            ATTN_STAMP(3 + 2 * t);
           }
         }
         if (ptx::elect_one_sync()) {
@@ -751,12 +683,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         extra_blocks = 0;
       }
     }
-#ifdef ATTN_PROFILE_WAITS
-    if (lane == 0 && p.trace) {
-      long long* out = reinterpret_cast<long long*>(p.trace) + blockIdx.x * 8;
-      out[0] = clock64() - t_start; out[1] = w_q; out[2] = w_kv; out[3] = w_p0; out[4] = w_p1; out[5] = w_sched;
-    }
-#endif
   } else if (warp == 2) {
     // --------------------------------------------------------------- scheduler
     if (ATTN_SETMAXNREG) ptx::setmaxnreg_dec<kOtherRegs>();
@@ -784,18 +710,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
     SchedReader<kCl> sr;
     uint32_t s_phase = 0, o_phase = 0, gblk = 0;
-#ifdef ATTN_CYCLES
-    // per-warp cycle account of the softmax chain, kept in registers and
-    // written once at exit: [S wait, ld, max, exps+stores, p_free wait,
-    // epilogue (incl. o_ready wait), o_ready wait, blocks]
-    long long cyc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    long long c_t = 0;
-#define ATTN_CYC_START() c_t = clock64();
-#define ATTN_CYC_ADD(i) { const long long c_n = clock64(); cyc[i] += c_n - c_t; c_t = c_n; }
-#else
-#define ATTN_CYC_START()
-#define ATTN_CYC_ADD(i)
-#endif
+    ATTN_CYC_DECL()
     [[maybe_unused]] uint32_t pf_phase = 0;
     while (true) {
       const int4 e = sr.next(ctrl, false);
@@ -812,9 +727,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       // keys of the last key block that exist (ragged N): local key k < tail_keys
       const int last_blk = p.nblk - 1;
       const int tail_lim = (p.N - last_blk * kBlockN - 1) - cbase;  // last block: local k visible iff k <= tail_lim
-#ifdef ATTN_TIMELINE
-      const bool first_unit = (gblk == 0);
-#endif
       float m = -INFINITY, l = 0.f;
       for (int j = 0; j < nt; ++j, ++gblk) {
         ATTN_CYC_START();
@@ -822,27 +734,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         ATTN_CYC_ADD(0);
         s_phase ^= 1;
         ptx::tc_fence_after();
-#ifdef ATTN_TIMELINE
-        long long* tls = (p.trace && blockIdx.x == 0 && quarter == 0 && lane == 0 && first_unit && j < 64)
-                             ? reinterpret_cast<long long*>(p.trace) + 600 + t * 200 + j * 3 : nullptr;
-        // every quarter's S wake-up and P h1 publication: [5120 + (t*4+quarter)*128 + 2j + {0,1}]
-        long long* tlq = (p.trace && blockIdx.x == 0 && lane == 0 && first_unit && j < 64)
-                             ? reinterpret_cast<long long*>(p.trace) + 5120 + (t * 4 + quarter) * 128 + 2 * j : nullptr;
-        if (tlq) tlq[0] = clock64();
-        // fine stamps: [s_wake, ld done, max done, P half 0, P half 1, sum done]
-        long long* tl2 = (p.trace && blockIdx.x == 0 && quarter == 0 && lane == 0 && first_unit && j < 64)
-                             ? reinterpret_cast<long long*>(p.trace) + 4096 + t * 512 + j * 8 : nullptr;
-        if (tls) tls[0] = clock64();
-        if (tl2) tl2[0] = clock64();
-#endif
-#ifdef ATTN_DEBUG_SKIP_SOFTMAX
-        __syncwarp();
-        if (kSepP && lane == 0) ptx::mbar_arrive(&ctrl->s_free[t]);
-        if (lane == 0)
-          for (int h = 0; h < kPParts; ++h) ptx::mbar_arrive(&ctrl->p_ready[t][h]);
-        l = 1.f;
-        continue;
-#endif
         uint32_t r[kCols];
         if constexpr (kCols == 128) ptx::tmem_ld128(trow + colS, r);
         else ptx::tmem_ld64(trow + colS, r);
@@ -851,9 +742,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&ctrl->s_free[t]);
         }
-#ifdef ATTN_TIMELINE
-        if (tl2) tl2[1] = clock64() + (r[0] & 0) + (r[kCols - 1] & 0);
-#endif
         // visible local keys are k <= lim: causal diagonal block (key <= query)
         // and/or the ragged last key block (key < N)
         int lim = kCols;
@@ -876,9 +764,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             mq[g4] = fmaxf(mq[g4], fmaxf(__uint_as_float(r[k + 2 * g4]), __uint_as_float(r[k + 2 * g4 + 1])));
         }
         float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
-#ifdef ATTN_TIMELINE
-        if (tl2) tl2[2] = clock64() + (long long)(mx == 12345.f);
-#endif
         if constexpr (kSplit == 2) {
           sred->red[t][quarter][hf][gblk & 1][lane] = mx;
           ptx::named_bar_sync(bar_id, 64);
@@ -955,22 +840,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           constexpr int kPc = kCols / kPParts / 2;  // packed P columns per slice
-#ifdef ATTN_TIMELINE
-          if (tl2 && (h == 0 || h == kPParts - 1)) tl2[6 + (h > 0)] = clock64() + (long long)(r[h * kPc] == 12345u);
-#endif
           if constexpr (kPc == 32) ptx::tmem_st32(trow + colP + h * 32, r + h * 32);
           else ptx::tmem_st16(trow + colP + h * 16, r + h * 16);
           ptx::tmem_wait_st();
           ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&ctrl->p_ready[t][h]);
-#ifdef ATTN_TIMELINE
-          if (h == 0 || h == kPParts - 1) {
-            if (tls) tls[1 + (h > 0)] = clock64();
-            if (tlq && h > 0) tlq[1] = clock64();
-            if (tl2) tl2[3 + (h > 0)] = clock64();
-          }
-#endif
         }
         };
         ATTN_CYC_ADD(2);
@@ -978,16 +853,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         else exp_block(std::false_type{});
         const float2 s01 = ptx::fadd2(sq[0], sq[1]), s23 = ptx::fadd2(sq[2], sq[3]);
         const float2 s4 = ptx::fadd2(s01, s23);
-#ifdef ATTN_TIMELINE
-        if (tl2) tl2[5] = clock64() + (long long)(s4.x == 12345.f);
-#endif
         const float sum = s4.x + s4.y;
         l = (j == 0) ? sum : fmaf(l, alpha, sum);
         m = m_use;
         ATTN_CYC_ADD(3);
-#ifdef ATTN_CYCLES
-        cyc[7] += 1;
-#endif
+        ATTN_CYC_COUNT(7);
       }
       ATTN_CYC_START();
       // ---- epilogue: O / l -> bf16 -> global
@@ -996,15 +866,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::named_bar_sync(bar_id, 64);
         l += sred->lsum[t][quarter][hf ^ 1][lane];
       }
-      {
-#ifdef ATTN_CYCLES
-        const long long c_o = clock64();
-#endif
-        ptx::mbar_wait(&ctrl->o_ready[t], o_phase);
-#ifdef ATTN_CYCLES
-        cyc[6] += clock64() - c_o;
-#endif
-      }
+      ATTN_CYC_TIMED(6, ptx::mbar_wait(&ctrl->o_ready[t], o_phase));
       o_phase ^= 1;
       ptx::tc_fence_after();
       const float inv_l = 1.f / l;
@@ -1039,34 +901,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::tc_fence_before();
       ATTN_CYC_ADD(5);
     }
-#ifdef ATTN_CYCLES
-    if (p.trace && lane == 0 && blockIdx.x < 64) {
-      long long* out = reinterpret_cast<long long*>(p.trace) + (blockIdx.x * 8 + (warp - 4)) * 8;
-      for (int i = 0; i < 8; ++i) out[i] = cyc[i];
-    }
-#endif
+    ATTN_CYC_WRITE(p.trace, warp - 4)
   } else {
     if (ATTN_SETMAXNREG) ptx::setmaxnreg_dec<kOtherRegs>();  // warp 3: idle
-#ifdef ATTN_TIMELINE
-    // timeline probe: when does each s_ready[0] phase (S_0(j) of the first
-    // unit) complete?  -> trace[3072 + j]
-    if (p.trace && blockIdx.x == 0 && lane == 0) {
-      long long* tq = reinterpret_cast<long long*>(p.trace) + 3072;
-      for (int k = 0; k < 64; ++k) {
-        uint32_t ok = 0;
-        while (!ok) {
-          asm volatile(
-              "{\n\t.reg .pred q;\n\t"
-              "mbarrier.test_wait.parity.acquire.cta.shared::cta.b64 q, [%1], %2;\n\t"
-              "selp.u32 %0, 1, 0, q;\n\t}"
-              : "=r"(ok)
-              : "r"(ptx::smem_u32(&ctrl->s_ready[0])), "r"((uint32_t)(k & 1))
-              : "memory");
-        }
-        tq[k] = clock64();
-      }
-    }
-#endif
   }
 
   ptx::tc_fence_before();

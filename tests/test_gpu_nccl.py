@@ -41,8 +41,8 @@ def test_nccl_world1_replicated_output_bit_identical():
     assert rep["allgather_backend"] == "nccl", rep
     assert rep["fwd_then_nccl_allgather_ms"] > 0 and rep["fused_peer_store_ms"] > 0
     assert rep["bit_identical"] is True
-    # communicator creation is logged (NCCL_DEBUG=INFO scoped to INIT by dist.init)
-    assert "NCCL INFO" in out.stdout + out.stderr
+    # NCCL itself ran and announced itself (NCCL_DEBUG=INFO scoped to INIT by dist.init)
+    assert "NCCL version" in out.stdout + out.stderr
 
 
 def test_nccl_world1_all_gather_heads_direct(tmp_path):

@@ -22,6 +22,16 @@ def test_topology_probe_two_dies():
         assert t["n_domains"] == 2 and sum(t["sms_per_domain"]) == t["num_sms"]
         assert t["lat_far_cyc"] - t["lat_near_cyc"] >= 8
         assert t["stable"]
+        # two dies of roughly half the SMs each (B200: 74 SMs per die, some fused off)
+        assert min(t["sms_per_domain"]) >= 60
+        # far_lines_cached_near is MEASURED: near lines
+        # re-read at about the near hit latency, and the flag follows the rule
+        # stated in include/attn_numa.h from the two re-read latencies
+        n2, f2 = t["lat_near_reread_cyc"], t["lat_far_reread_cyc"]
+        assert n2 > 0 and f2 > 0
+        assert abs(n2 - t["lat_near_cyc"]) <= 0.2 * t["lat_near_cyc"]
+        rule = int((f2 - n2) < 0.5 * (t["lat_far_cyc"] - t["lat_near_cyc"]))
+        assert t["far_lines_cached_near"] == rule
 
 
 def _trace_run(B, Hq, Hkv, N, d, causal, mapping):
