@@ -49,6 +49,10 @@ WORKLOADS = {
 }
 METRIC = "attention fwd TFLOP/s (% of bf16 peak) and L2 hit rate by mapping, 1/2/4/8 B200"
 MAPS = ("block_first", "head_first", "swizzled_head_first", "swizzled_block_first")
+# swizzled head-first at the paper's literal grain (one die per ACC) beside the
+# library's choice (R23: ACCs shared by the dies when the dies' K/V
+# footprints overflow the shared L2); reported in by_mapping
+VARIANT_MAPS = MAPS + ("swizzled_head_first:per_die",)
 # ncu metrics of the per-mapping evidence (north star: L2 hit rate, tensor-pipe
 # utilisation, HBM GB/s); R13: sector hit rate over all ops plus the read-only rate
 NCU_METRICS = ("gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
@@ -163,7 +167,7 @@ def ncu_child(a):
     o = torch.empty_like(q)
     api.attn_init(a.device)
     for spec in a.variants.split(";"):
-        m, cl, order = spec.split(":")
+        m, cl, order = spec.split("/")
         api.attn_fwd(q, k, v, o, causal=bool(causal), scale=1.0 / math.sqrt(d), mapping=m, order=order,
                      cluster=cl == "1")
         torch.cuda.synchronize()
@@ -187,7 +191,7 @@ def ncu_measure(shape, variants, device: int, timeout_s: float):
     Returns ({variant key: fields}, provenance dict)."""
     ncu = "/usr/local/cuda/bin/ncu" if os.path.exists("/usr/local/cuda/bin/ncu") else "ncu"
     log = os.path.join("/tmp", f"attn_bench_ncu_{os.getpid()}.csv")
-    spec = ";".join(f"{m}:{int(cl)}:{o}" for (m, cl, o) in variants)
+    spec = ";".join(f"{m}/{int(cl)}/{o}" for (m, cl, o) in variants)
     cmd = [ncu, "--csv", "--print-units", "base", "--log-file", log, "--clock-control", "none",
            "--cache-control", "all", "-k", "regex:attn_fwd_sm100", "--metrics", ",".join(NCU_METRICS),
            sys.executable, os.path.join(ROOT, "bench.py"), "--ncu-child", ",".join(str(int(x)) for x in shape),
@@ -326,12 +330,13 @@ def run_ours(a):
     main_var = (a.mapping, bool(a.cluster) and a.pass_ == "fwd", a.order)
     sampler = ClockSampler(local)
     ms_step, ms_kernel, launches = timed(main_var, a.steps, a.warmup, sampler)
+    shf_grain = "shared" if api.attn_last_launch_info().get("shf_acc_shared") else "per_die"
     clocks = sampler.summary()
     value = flops_job / (ms_step * 1e-3) / 1e12
 
     # every mapping on the same inputs in the same run, plain and (forward) as
     # CTA-pair clusters; fewer steps each
-    variants = [(m, cl, "ascending") for m in MAPS for cl in ((False, True) if a.pass_ == "fwd" else (False,))]
+    variants = [(m, cl, "ascending") for m in VARIANT_MAPS for cl in ((False, True) if a.pass_ == "fwd" else (False,))]
     if main_var not in variants:
         variants.append(main_var)
     by_mapping = {}
@@ -417,6 +422,8 @@ def run_ours(a):
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (i.i.d. N(0,1) rounded to bf16, seeded per head)",
         "config": {"workload": a.workload, "B": B, "Hq": Hq_job, "Hkv": Hkv_job, "N": N, "d": d, "causal": causal,
                    "mapping": a.mapping, "order": a.order, "pass": a.pass_, "heads_per_gpu": hq,
+                   "shf_acc_grain": (shf_grain + " (DESIGN.md R23)") if a.mapping.startswith("swizzled_head_first")
+                   else None,
                    "cluster_multicast": main_var[1],
                    "parallelism": f"heads sharded over {world} GPU(s), no data-path collective",
                    "l2": l2_note, "flop_convention": ("4*B*Hq*N^2*d, causal x0.5" if a.pass_ == "fwd" else
@@ -718,7 +725,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default="C5", choices=sorted(WORKLOADS))
-    ap.add_argument("--mapping", default="swizzled_head_first", choices=MAPS)
+    ap.add_argument("--mapping", default="swizzled_head_first", choices=VARIANT_MAPS + ("swizzled_head_first:shared",))
     ap.add_argument("--order", default="ascending", choices=("ascending", "descending", "alternate"),
                     help="unit order of the value variant (ATTN_ORDER_*); by_mapping uses ascending")
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))

@@ -109,6 +109,23 @@ typedef enum {
  * non-cluster path. */
 #define ATTN_CLUSTER_MULTICAST 0x200
 
+/* OR into `mapping` with ATTN_MAP_SWIZZLED_HEAD_FIRST: the grain of "one
+ * ACC per die".  B200 reading R23: the two
+ * dies share ONE L2 (lines homed by address; the probe measures that a far
+ * line is not replicated near, far_lines_cached_near = 0), so serving one ACC
+ * per die keeps n_domains ACC K/V footprints live in that L2 at once.
+ *   ATTN_SHF_ACC_SHARED   every ACC is served by all dies together: of every
+ *                         S = sum(sms_per_domain) consecutive units of the
+ *                         head-major order, die d's queue takes its
+ *                         sms_per_domain[d] units (per-die queues, stealing);
+ *   ATTN_SHF_ACC_PER_DIE  the paper's literal grain (one die per ACC) always;
+ *   neither               the library decides per call with
+ *                         attn_shf_acc_shared(n_domains, N, d, l2_bytes).
+ * Schedule only: never changes the result bits.  Exclusive with each other;
+ * ignored by the other mappings. */
+#define ATTN_SHF_ACC_SHARED 0x800
+#define ATTN_SHF_ACC_PER_DIE 0x1000
+
 typedef enum {
   ATTN_OK = 0,
   ATTN_ERR_INVALID_VALUE = 1, /* null pointer, size <= 0, Hq % Hkv != 0, bad mapping value,
@@ -288,9 +305,16 @@ ATTN_API int attn_set_schedule_trace(int device, void* dev_buf, long long capaci
 ATTN_API int attn_schedule_order(int B, int Hq, int Hkv, int N, int mapping, int n_domains, const int* sms_per_domain,
                         int32_t* out, long long capacity, int* n_queues, int* queue_len);
 
-/* Launch geometry of the last successful attn_fwd* on this thread. */
+/* The rule swizzled head-first applies when neither ATTN_SHF_ACC_* flag is
+ * given (R23): 1 (share every ACC among the dies) iff n_domains > 1,
+ * l2_bytes > 0 and n_domains * (K + V bytes of one KV head = 4*N*d) >
+ * l2_bytes / 2, else 0.  Pure function; no device access. */
+ATTN_API int attn_shf_acc_shared(int n_domains, int N, int d, long long l2_bytes);
+
+/* Launch geometry of the last successful attn_fwd* on this thread;
+ * shf_acc_shared = 1 if swizzled head-first ran with ACCs shared by all dies. */
 typedef struct {
-  int grid, block, smem_bytes, units, n_queues, kernel_launches;
+  int grid, block, smem_bytes, units, n_queues, kernel_launches, shf_acc_shared;
 } attn_launch_info_t;
 ATTN_API int attn_last_launch_info(attn_launch_info_t* out);
 

@@ -140,14 +140,26 @@ def block_major_tiles(B: int, Hq: int, nblk: int) -> List[Tile]:
     return [(b, h, k) for b in range(B) for k in range(nblk) for h in range(Hq)]
 
 
+def shf_acc_shared(n_domains: int, N: int, d: int, l2_bytes: int) -> bool:
+    """R23 (B200 reading of P:259-270): the dies share one L2, so swizzled
+    head-first keeps n_domains ACC footprints (K and V of one KV head:
+    2 tensors x N x d x 2 bytes each) live in it at once; when together they
+    exceed half of the L2, each ACC is shared by all dies instead."""
+    footprint_one_acc = 2 * N * d * 2
+    return n_domains > 1 and l2_bytes > 0 and n_domains * footprint_one_acc > l2_bytes // 2
+
+
 def build_queues(mapping: str, B: int, Hq: int, Hkv: int, nblk: int,
-                 domain_sizes: Sequence[int]) -> List[List[Tile]]:
+                 domain_sizes: Sequence[int], shared_acc: bool = False) -> List[List[Tile]]:
     """Ordered work queues a B200 persistent grid pops from.
 
     block_first / head_first: one queue shared by every SM of every die
     (the B200 analogue of round-robin dispatch: consecutive tiles of a head
     land on SMs of both dies).  swizzled_head_first: one queue per die
-    (R8), each die serving its ACCs one at a time in head-major order.
+    (R8), each die serving its ACCs one at a time in head-major order; with
+    shared_acc (R23) all dies serve the same ACC: of every S = sum(sizes)
+    consecutive tiles of the head-major list, die d takes sizes[d] of them
+    (the ones after the first sizes[0] + ... + sizes[d-1]).
     """
     if mapping == BLOCK_FIRST:
         return [block_major_tiles(B, Hq, nblk)]
@@ -174,6 +186,15 @@ def build_queues(mapping: str, B: int, Hq: int, Hkv: int, nblk: int,
     if D == 1:
         return [head_major_tiles(B, Hq, nblk)]
     queues: List[List[Tile]] = [[] for _ in range(D)]
+    if shared_acc:
+        S = sum(domain_sizes)
+        first_slot = [sum(domain_sizes[:e]) for e in range(D)]
+        for p, tile in enumerate(head_major_tiles(B, Hq, nblk)):
+            slot = p % S
+            for d in range(D):
+                if first_slot[d] <= slot < first_slot[d] + domain_sizes[d]:
+                    queues[d].append(tile)
+        return queues
     if Hkv >= D:
         # Fig. 7 generalised: per batch item, ACCs [cut_d, cut_{d+1}) -> die d.
         cuts = _prop_cuts(Hkv, domain_sizes)

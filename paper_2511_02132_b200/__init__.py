@@ -7,14 +7,14 @@ or swizzled head-first order.  This package is a thin ctypes binding.
 """
 from .api import (AttnError, MAPPING_NAMES, MAPPINGS, attn_bwd, attn_bwd_host, attn_fwd, attn_fwd_host, attn_fwd_lse, attn_fwd_replicated,
                   attn_init, ipc_close, ipc_get_handle, ipc_open,
-                  attn_last_launch_info, attn_schedule_order, attn_set_schedule_trace,
+                  attn_last_launch_info, attn_schedule_order, attn_set_schedule_trace, attn_shf_acc_shared,
                   attn_set_topology_override, attn_shutdown, attn_topology, attn_version,
                   decode_trace, trace_buffer)
 
 __all__ = [
     "AttnError", "MAPPINGS", "MAPPING_NAMES", "attn_bwd", "attn_bwd_host", "attn_fwd", "attn_fwd_host", "attn_fwd_lse", "attn_fwd_replicated", "attn_init", "ipc_close",
     "ipc_get_handle", "ipc_open",
-    "attn_last_launch_info", "attn_schedule_order", "attn_set_schedule_trace",
+    "attn_last_launch_info", "attn_schedule_order", "attn_set_schedule_trace", "attn_shf_acc_shared",
     "attn_set_topology_override", "attn_shutdown", "attn_topology", "attn_version",
     "decode_trace", "trace_buffer",
 ]

@@ -19,7 +19,7 @@ EXPORTS = (
     "attn_fwd", "attn_fwd_stream", "attn_fwd_lse", "attn_bwd", "attn_fwd_host", "attn_bwd_host", "attn_set_stream", "attn_init", "attn_topology",
     "attn_set_topology_override", "attn_set_schedule_trace", "attn_schedule_order",
     "attn_last_launch_info", "attn_status_string", "attn_last_error", "attn_version", "attn_shutdown",
-    "attn_fwd_replicated", "attn_ipc_get_handle", "attn_ipc_open", "attn_ipc_close",
+    "attn_fwd_replicated", "attn_ipc_get_handle", "attn_ipc_open", "attn_ipc_close", "attn_shf_acc_shared",
 )
 
 
@@ -51,7 +51,8 @@ class TraceRec(ctypes.Structure):
 
 class LaunchInfo(ctypes.Structure):
     _fields_ = [("grid", ctypes.c_int), ("block", ctypes.c_int), ("smem_bytes", ctypes.c_int),
-                ("units", ctypes.c_int), ("n_queues", ctypes.c_int), ("kernel_launches", ctypes.c_int)]
+                ("units", ctypes.c_int), ("n_queues", ctypes.c_int), ("kernel_launches", ctypes.c_int),
+                ("shf_acc_shared", ctypes.c_int)]
 
 
 class IpcHandle(ctypes.Structure):
@@ -90,10 +91,11 @@ def load():
     lib.attn_ipc_get_handle.argtypes = [vp, ctypes.POINTER(IpcHandle)]
     lib.attn_ipc_open.argtypes = [ctypes.POINTER(IpcHandle), ctypes.POINTER(ctypes.c_void_p)]
     lib.attn_ipc_close.argtypes = [vp]
+    lib.attn_shf_acc_shared.argtypes = [i32, i32, i32, ctypes.c_longlong]
     for f in ("attn_fwd", "attn_fwd_stream", "attn_fwd_lse", "attn_bwd", "attn_fwd_host", "attn_bwd_host", "attn_set_stream", "attn_init", "attn_topology",
               "attn_set_topology_override", "attn_set_schedule_trace", "attn_schedule_order",
               "attn_last_launch_info", "attn_fwd_replicated", "attn_ipc_get_handle", "attn_ipc_open",
-              "attn_ipc_close"):
+              "attn_ipc_close", "attn_shf_acc_shared"):
         getattr(lib, f).restype = i32
     lib.attn_status_string.argtypes = [i32]
     lib.attn_status_string.restype = ctypes.c_char_p

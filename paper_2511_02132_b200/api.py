@@ -37,10 +37,20 @@ ORDER_DESCENDING = 0x100  # include/attn_numa.h ATTN_ORDER_DESCENDING
 CLUSTER_MULTICAST = 0x200  # include/attn_numa.h ATTN_CLUSTER_MULTICAST
 ORDER_ALTERNATE = 0x400  # include/attn_numa.h ATTN_ORDER_ALTERNATE
 ORDERS = {"ascending": 0, "descending": ORDER_DESCENDING, "alternate": ORDER_ALTERNATE}
+SHF_ACC_SHARED = 0x800  # include/attn_numa.h ATTN_SHF_ACC_SHARED
+SHF_ACC_PER_DIE = 0x1000  # include/attn_numa.h ATTN_SHF_ACC_PER_DIE
+# "swizzled_head_first:shared" / ":per_die" force the SHF ACC grain (R23); no suffix = library rule
+SHF_ACC = {"": 0, "shared": SHF_ACC_SHARED, "per_die": SHF_ACC_PER_DIE}
 
 
 def _mapping_id(mapping, order: str = "ascending", cluster: bool = False) -> int:
-    m = mapping if isinstance(mapping, int) else MAPPINGS[str(mapping).lower()]
+    if isinstance(mapping, int):
+        m = mapping
+    else:
+        name, _, grain = str(mapping).lower().partition(":")
+        if grain not in SHF_ACC:
+            raise ValueError("mapping suffix must be ':shared' or ':per_die'")
+        m = MAPPINGS[name] | SHF_ACC[grain]
     if order not in ORDERS:
         raise ValueError("order must be 'ascending', 'descending' or 'alternate'")
     m |= ORDERS[order]
@@ -309,6 +319,11 @@ def attn_schedule_order(B: int, Hq: int, Hkv: int, N: int, mapping, sms_per_doma
             w += 1
         queues.append(q)
     return queues
+
+
+def attn_shf_acc_shared(n_domains: int, N: int, d: int, l2_bytes: int) -> bool:
+    """The library's SHF ACC-grain rule (C-ABI attn_shf_acc_shared, R23)."""
+    return bool(_lib.load().attn_shf_acc_shared(n_domains, N, d, l2_bytes))
 
 
 def attn_last_launch_info() -> Dict:

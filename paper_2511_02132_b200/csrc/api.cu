@@ -436,9 +436,13 @@ int validate(const void* q, const void* k, const void* v, void* o, int B, int Hq
   if (!q || !k || !v || !o) return fail(ATTN_ERR_INVALID_VALUE, "null pointer");
   if (B <= 0 || Hq <= 0 || Hkv <= 0 || N <= 0 || d <= 0) return fail(ATTN_ERR_INVALID_VALUE, "size <= 0");
   if (Hq % Hkv != 0) return fail(ATTN_ERR_INVALID_VALUE, "Hq % Hkv != 0 (non-uniform GQA groups)");
-  if ((mapping & ~(kMapMask | kOrderDescending | kOrderAlternate | ATTN_CLUSTER_MULTICAST)) || (mapping & kMapMask) > 3)
+  if ((mapping & ~(kMapMask | kOrderDescending | kOrderAlternate | ATTN_CLUSTER_MULTICAST | kShfAccShared |
+                   kShfAccPerDie)) || (mapping & kMapMask) > 3)
     return fail(ATTN_ERR_INVALID_VALUE,
-                "mapping not in {0,1,2,3} (| ATTN_ORDER_DESCENDING | ATTN_ORDER_ALTERNATE | ATTN_CLUSTER_MULTICAST)");
+                "mapping not in {0,1,2,3} (| ATTN_ORDER_DESCENDING | ATTN_ORDER_ALTERNATE | ATTN_CLUSTER_MULTICAST | "
+                "ATTN_SHF_ACC_SHARED | ATTN_SHF_ACC_PER_DIE)");
+  if ((mapping & kShfAccShared) && (mapping & kShfAccPerDie))
+    return fail(ATTN_ERR_INVALID_VALUE, "ATTN_SHF_ACC_SHARED and ATTN_SHF_ACC_PER_DIE are exclusive");
   if (!std::isfinite(scale)) return fail(ATTN_ERR_INVALID_VALUE, "non-finite scale");
   const size_t qb = (size_t)B * Hq * N * d * 2, kb = (size_t)B * Hkv * N * d * 2;
   if (overlaps(o, qb, q, qb) || overlaps(o, qb, k, kb) || overlaps(o, qb, v, kb))
@@ -614,6 +618,11 @@ int fwd_impl(const void* q, const void* k, const void* v, void* o, int B, int Hq
     kp.h_off = 0;
   }
   kp.lse = lse;
+  // R23: swizzled head-first shares each ACC among the dies when the dies'
+  // ACC footprints would overflow the shared L2 (unless forced either way)
+  if ((mapping & kMapMask) == ATTN_MAP_SWIZZLED_HEAD_FIRST && !(mapping & (kShfAccShared | kShfAccPerDie)) &&
+      shf_acc_shared(st.active.n_domains, N, d, st.measured.l2_bytes))
+    mapping |= kShfAccShared;
   if (!build_sched(mapping, B, Hsched, Hkv, Usched, st.active.n_domains, st.active.sms_per_domain, kp.sched))
     return fail(ATTN_ERR_INVALID_VALUE, "cannot build the schedule");
   kp.counters = st.d_counters + (size_t)counter_slot(st, stream) * kCounterInts;
@@ -639,6 +648,8 @@ int fwd_impl(const void* q, const void* k, const void* v, void* o, int B, int Hq
   if (rc != ATTN_OK) return rc;
   g_info.units = total;
   g_info.n_queues = kp.sched.n_queues;
+  g_info.shf_acc_shared = ((mapping & kMapMask) == ATTN_MAP_SWIZZLED_HEAD_FIRST && (mapping & kShfAccShared) &&
+                           kp.sched.n_queues > 1) ? 1 : 0;
   g_info.kernel_launches = 1;
   return ATTN_OK;
 }
@@ -1110,6 +1121,10 @@ int attn_schedule_order(int B, int Hq, int Hkv, int N, int mapping, int n_domain
   }
   *n_queues = sp.n_queues;
   return ATTN_OK;
+}
+
+int attn_shf_acc_shared(int n_domains, int N, int d, long long l2_bytes) {
+  return shf_acc_shared(n_domains, N, d, l2_bytes) ? 1 : 0;
 }
 
 int attn_last_launch_info(attn_launch_info_t* out) {

@@ -16,6 +16,11 @@
 //   kind 3  strided groups, block-major (Swizzled Block-first, P:236-243,
 //           S:172): queue d holds the KV groups g = h_lo + i*stride
 //           (i < n_groups) in order for b, for u, for g, for the G heads of g.
+//   kind 4  interleaved head-major slots (Swizzled Head-first with the ACC
+//           shared by all dies, R23): of every `stride` consecutive
+//           units of the head-major list, queue d holds the h_cnt units at
+//           offsets [start, start + h_cnt):
+//           hm = (pos / h_cnt) * stride + start + pos % h_cnt
 // Block-first and head-first use ONE queue popped by every SM of every die;
 // swizzled head-first uses one queue per die (reading R8).
 #pragma once
@@ -34,12 +39,13 @@ namespace attn {
 constexpr int kMaxQueues = 8;
 
 struct QueueDesc {
-  int kind;    // 0 block-major range, 1 head-major range, 2 per-batch head range, 3 strided groups
-  int start;   // first position (kinds 0, 1)
+  int kind;    // 0 block-major range, 1 head-major range, 2 per-batch head range, 3 strided groups,
+               // 4 interleaved head-major slots
+  int start;   // first position (kinds 0, 1); kind 4: first slot of the period
   int len;     // number of units in the queue
   int h_lo;    // kind 2: first query head; kind 3: first KV group
-  int h_cnt;   // kind 2: query heads per batch item; kind 3: number of KV groups
-  int stride;  // kind 3: KV-group stride (= number of dies)
+  int h_cnt;   // kind 2: query heads per batch item; kind 3: number of KV groups; kind 4: slots per period
+  int stride;  // kind 3: KV-group stride (= number of dies); kind 4: period (units)
   int G;       // kind 3: query heads per KV group
 };
 
@@ -58,8 +64,8 @@ ATTN_HD void decode_unit(const QueueDesc& qd, int pos, int Hq, int U, int& b, in
     const int r = p % (U * Hq);
     u = r / Hq;
     h = r % Hq;
-  } else if (qd.kind == 1) {
-    const int hm = qd.start + pos;
+  } else if (qd.kind == 1 || qd.kind == 4) {
+    const int hm = (qd.kind == 1) ? qd.start + pos : (pos / qd.h_cnt) * qd.stride + qd.start + pos % qd.h_cnt;
     b = hm / (Hq * U);
     h = (hm / U) % Hq;
     u = hm % U;
@@ -92,10 +98,26 @@ inline int prop_cut(long long total, const int* sizes, int n, int d) {
 // descending unit order inside every (b, h) (applied identically to every
 // mapping; the paper's order is ascending); bit 10 = alternate the unit
 // direction per queue (queue d descending iff d is odd; single-queue
-// mappings are unaffected) -- see include/attn_numa.h ATTN_ORDER_ALTERNATE.
+// mappings are unaffected) -- see include/attn_numa.h ATTN_ORDER_ALTERNATE;
+// bit 11 = SHF with every ACC shared by all dies (kind-4 queues), bit 12 =
+// SHF with one die per ACC even where the library would share it (R23).
 constexpr int kMapMask = 0xff;
 constexpr int kOrderDescending = 0x100;
 constexpr int kOrderAlternate = 0x400;
+constexpr int kShfAccShared = 0x800;
+constexpr int kShfAccPerDie = 0x1000;
+
+// DESIGN.md R23 (B200 reading of P:259-270): the dies share ONE L2 (lines
+// homed by address, far lines not replicated near: the probe's
+// far_lines_cached_near = 0), so "each die serves one ACC at a time" keeps
+// n_domains ACC K/V footprints live in that one L2.  When those footprints
+// exceed half of it (the capacity sweep: SHF's DRAM
+// bytes leave head-first's between 2 x 32 and 2 x 48 MiB per ACC on the
+// 126 MiB L2), swizzled head-first shares each ACC among the dies instead.
+ATTN_HD bool shf_acc_shared(int n_domains, long long N, int d, long long l2_bytes) {
+  const long long kv_acc = 2ll * N * d * 2;  // K and V of one KV head, bf16
+  return n_domains > 1 && l2_bytes > 0 && (long long)n_domains * kv_acc > l2_bytes / 2;
+}
 
 // Per-queue direction mask of an order argument for n_queues queues.
 ATTN_HD int direction_mask(int mapping_arg, int n_queues) {
@@ -109,7 +131,7 @@ ATTN_HD int direction_mask(int mapping_arg, int n_queues) {
 inline bool build_queues(int mapping_arg, int B, int Hq, int Hkv, int U, int n_domains, const int* sms_per_domain,
                          SchedParams& sp) {
   sp = SchedParams{};
-  if (mapping_arg & ~(kMapMask | kOrderDescending | kOrderAlternate)) return false;
+  if (mapping_arg & ~(kMapMask | kOrderDescending | kOrderAlternate | kShfAccShared | kShfAccPerDie)) return false;
   const int mapping = mapping_arg & kMapMask;
   if (B <= 0 || Hq <= 0 || Hkv <= 0 || U <= 0 || Hq % Hkv != 0) return false;
   if (n_domains < 1 || n_domains > kMaxQueues) return false;
@@ -127,6 +149,23 @@ inline bool build_queues(int mapping_arg, int B, int Hq, int Hkv, int U, int n_d
   sp.n_queues = D;
   sp.steal = 1;
   for (int d = 0; d < D; ++d) sp.queue_of_domain[d] = d;
+  if (mapping == 2 && (mapping_arg & kShfAccShared)) {
+    // R23: every die takes its SM share of each period of S consecutive
+    // head-major units, so all dies serve the same ACC at the same time
+    int S = 0;
+    for (int d = 0; d < D; ++d) S += sms_per_domain[d];
+    if (S <= 0) return false;
+    int c = 0;
+    for (int d = 0; d < D; ++d) {
+      const int sd = sms_per_domain[d];
+      if (sd < 0) return false;
+      const int full = total / S, rem = total % S;
+      const int tail = rem > c ? (rem - c < sd ? rem - c : sd) : 0;
+      sp.q[d] = QueueDesc{4, c, full * sd + tail, 0, sd, S, 0};
+      c += sd;
+    }
+    return true;
+  }
   if (mapping == 3) {
     for (int d = 0; d < D; ++d) {
       const int ng = (Hkv > d) ? (Hkv - d + D - 1) / D : 0;  // groups g = d, d + D, ...

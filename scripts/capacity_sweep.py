@@ -27,6 +27,10 @@ VARIANTS = {
     "hf": ("head_first", "ascending", False),
     "shf": ("swizzled_head_first", "ascending", False),
     "shf_alt": ("swizzled_head_first", "alternate", False),
+    "shf_pd": ("swizzled_head_first:per_die", "ascending", False),   # the paper's grain, forced
+    "shf_sh": ("swizzled_head_first:shared", "ascending", False),    # R23 grain, forced
+    "shf_pd_cl": ("swizzled_head_first:per_die", "ascending", True),
+    "shf_sh_cl": ("swizzled_head_first:shared", "ascending", True),
     "bf": ("block_first", "ascending", False),
     "hf_cl": ("head_first", "ascending", True),
     "shf_cl": ("swizzled_head_first", "ascending", True),

@@ -48,7 +48,7 @@ def _fwd(lib, q=1 << 20, k=2 << 20, v=3 << 20, o=4 << 20, B=1, Hq=2, Hkv=2, N=12
 
 @pytest.mark.parametrize("kw,status", [
     (dict(q=0), 1), (dict(o=0), 1), (dict(B=0), 1), (dict(N=-1), 1), (dict(Hq=6, Hkv=4), 1),
-    (dict(mapping=4), 1), (dict(mapping=-1), 1), (dict(mapping=0x800), 1), (dict(mapping=0x404), 1), (dict(mapping=0x204), 1), (dict(mapping=0x104), 1), (dict(scale=float("nan")), 1), (dict(scale=float("inf")), 1),
+    (dict(mapping=4), 1), (dict(mapping=-1), 1), (dict(mapping=0x2000), 1), (dict(mapping=0x804), 1), (dict(mapping=0x404), 1), (dict(mapping=0x204), 1), (dict(mapping=0x104), 1), (dict(scale=float("nan")), 1), (dict(scale=float("inf")), 1),
     (dict(d=100), 2), (dict(d=136), 2), (dict(scale=-0.5), 2), (dict(q=(1 << 20) + 8), 2),
     (dict(o=(1 << 20) + 64), 1),   # o overlaps q
 ])
@@ -83,6 +83,37 @@ def test_schedule_order_matches_oracle(lib, mapping):
         got = api.attn_schedule_order(B, Hq, Hkv, N, mapping, sizes)
         want = om.build_queues(mapping, B, Hq, Hkv, U, sizes)
         assert got == want, (mapping, B, Hq, Hkv, N, sizes)
+
+
+@pytest.mark.parametrize("grain", ["shared", "per_die"])
+def test_schedule_order_shf_grain_matches_oracle(lib, grain):
+    rng = random.Random(29)
+    for _ in range(60):
+        Hkv = rng.choice([1, 2, 3, 4, 8, 16])
+        Hq = Hkv * rng.choice([1, 2, 4])
+        B, N = rng.randint(1, 3), 128 * rng.randint(1, 12)
+        sizes = [rng.randint(60, 80) for _ in range(rng.randint(1, 3))]
+        U = (N + 255) // 256
+        got = api.attn_schedule_order(B, Hq, Hkv, N, "swizzled_head_first:" + grain, sizes)
+        want = om.build_queues(om.SWIZZLED_HEAD_FIRST, B, Hq, Hkv, U, sizes, shared_acc=grain == "shared")
+        assert got == want, (grain, B, Hq, Hkv, N, sizes)
+    # small dies, so the interleave period is shorter than a head
+    got = api.attn_schedule_order(1, 2, 2, 128 * 6, "swizzled_head_first:shared", [2, 1])
+    assert got == om.build_queues(om.SWIZZLED_HEAD_FIRST, 1, 2, 2, 3, [2, 1], shared_acc=True)
+
+
+def test_shf_acc_rule_matches_oracle(lib):
+    for D in (1, 2, 4):
+        for N in (128, 8192, 32768, 64512, 64513, 65536, 98304, 131072, 262144):
+            for d in (56, 64, 128):
+                for l2 in (0, 50 << 20, 132120576):
+                    assert api.attn_shf_acc_shared(D, N, d, l2) == om.shf_acc_shared(D, N, d, l2), (D, N, d, l2)
+
+
+def test_shf_grain_flags_exclusive(lib):
+    fake = [(i + 1) << 20 for i in range(4)]
+    rc = lib.attn_fwd(*fake, 1, 2, 2, 128, 64, 0, 0.125, 2 | 0x800 | 0x1000)
+    assert rc == 1 and b"exclusive" in lib.attn_last_error()
 
 
 def test_schedule_order_descending_matches_oracle(lib):

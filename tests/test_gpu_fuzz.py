@@ -19,7 +19,7 @@ from test_gpu_parity import MAX_TOL, MEAN_TOL
 
 pytestmark = pytest.mark.gpu
 
-MAPS = ("block_first", "head_first", "swizzled_head_first", "swizzled_block_first")
+MAPS = ("block_first", "head_first", "swizzled_head_first", "swizzled_block_first", "swizzled_head_first:shared")
 
 
 def _cases(n, seed):

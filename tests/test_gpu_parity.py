@@ -18,7 +18,8 @@ pytestmark = pytest.mark.gpu
 
 MAX_TOL = 2e-2
 MEAN_TOL = 2e-3
-MAPS = ("block_first", "head_first", "swizzled_head_first", "swizzled_block_first")
+MAPS = ("block_first", "head_first", "swizzled_head_first", "swizzled_block_first",
+        "swizzled_head_first:shared")  # R23 grain, forced even where the rule would not pick it
 
 
 def _check(out: torch.Tensor, ref: np.ndarray, what: str):

@@ -8,7 +8,8 @@ import torch
 
 from oracle import attn as oa
 from oracle import mapping as om
-from paper_2511_02132_b200 import (attn_fwd, attn_fwd_host, attn_set_schedule_trace, attn_set_topology_override,
+from paper_2511_02132_b200 import (attn_fwd, attn_fwd_host, attn_last_launch_info, attn_set_schedule_trace,
+                                   attn_set_topology_override, attn_shf_acc_shared,
                                    attn_topology, decode_trace, synth, trace_buffer)
 
 pytestmark = pytest.mark.gpu
@@ -45,7 +46,8 @@ def _trace_run(B, Hq, Hkv, N, d, causal, mapping):
     return decode_trace(buf), o
 
 
-@pytest.mark.parametrize("mapping", ["block_first", "head_first", "swizzled_head_first"])
+@pytest.mark.parametrize("mapping", ["block_first", "head_first", "swizzled_head_first",
+                                     "swizzled_head_first:shared"])
 def test_every_unit_processed_exactly_once(mapping):
     B, Hq, Hkv, N, d = 2, 16, 4, 2048, 128
     tr, _ = _trace_run(B, Hq, Hkv, N, d, True, mapping)
@@ -77,6 +79,43 @@ def test_swizzled_head_first_colocates_accs_on_device():
         for (b, h, u) in q:
             rec = tr[(b * Hq + h) * (N // 256) + u]
             assert int(rec[5]) == qi
+
+
+def test_shared_acc_grain_on_device():
+    """R23: with the ACC shared, every ACC's units run on SMs of every die and
+    each unit is popped from the queue the mapping reference puts it in
+    (or stolen at the tail); the result is bit-identical to the per-die grain."""
+    t = attn_topology(0)
+    if t["n_domains"] < 2:
+        pytest.skip("probe found one domain")
+    B, Hq, Hkv, N, d = 1, 8, 8, 16384, 128
+    tr, o_sh = _trace_run(B, Hq, Hkv, N, d, True, "swizzled_head_first:shared")
+    _, o_pd = _trace_run(B, Hq, Hkv, N, d, True, "swizzled_head_first:per_die")
+    assert torch.equal(o_sh.view(torch.int16), o_pd.view(torch.int16))
+    U = N // 256
+    queues = om.build_queues("swizzled_head_first", B, Hq, Hkv, U, t["sms_per_domain"], shared_acc=True)
+    doms = collections.defaultdict(set)
+    for qi, q in enumerate(queues):
+        for (b, h, u) in q:
+            rec = tr[(b * Hq + h) * U + u]
+            assert int(rec[5]) == qi or int(rec[6]) == 1
+            doms[(b, h)].add(int(rec[4]))
+    assert all(len(s) == 2 for s in doms.values())
+
+
+def test_shf_grain_rule_applied_by_the_library():
+    """attn_fwd with plain SHF picks the R23 grain from the probe's L2 size:
+    per-die at 2 x 16 MiB of K/V, shared at 2 x 64 MiB (BASELINE C5's N)."""
+    t = attn_topology(0)
+    for N, want in ((32768, False), (131072, True)):
+        q, k, v = synth.make_qkv(1, 1, 1, N, 128, base=0, device="cuda")
+        attn_fwd(q, k, v, causal=True, mapping="swizzled_head_first")
+        torch.cuda.synchronize()
+        rule = attn_shf_acc_shared(t["n_domains"], N, 128, t["l2_bytes"])
+        assert attn_last_launch_info()["shf_acc_shared"] == int(rule and t["n_domains"] > 1)
+        if t["n_domains"] == 2 and t["l2_bytes"] >= 100 << 20:
+            assert rule == want
+        del q, k, v
 
 
 def test_head_first_spreads_heads_over_both_dies():

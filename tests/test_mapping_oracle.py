@@ -207,3 +207,50 @@ def test_alternate_worked_example():
     ]
     hf = om.build_queues(om.HEAD_FIRST, 1, 2, 2, 2, [74, 74])
     assert om.alternate(hf, 2) == [[(0, 0, 0), (0, 0, 1), (0, 1, 0), (0, 1, 1)]]
+
+
+def test_shared_acc_worked_example():
+    """DESIGN.md R23 written out by hand: Z=1, Hq=Hkv=2, three query blocks,
+    dies of 2 and 1 SMs (S = 3).  Head-major list (0,0,0) (0,0,1) (0,0,2)
+    (0,1,0) (0,1,1) (0,1,2): die 0 takes slots 0-1 of every 3, die 1 slot 2."""
+    q = om.build_queues(om.SWIZZLED_HEAD_FIRST, 1, 2, 2, 3, [2, 1], shared_acc=True)
+    assert q == [[(0, 0, 0), (0, 0, 1), (0, 1, 0), (0, 1, 1)],
+                 [(0, 0, 2), (0, 1, 2)]]
+    # a ragged last period: 5 tiles over dies of 2 and 2 -> die 0 {0,1,4}, die 1 {2,3}
+    q = om.build_queues(om.SWIZZLED_HEAD_FIRST, 1, 1, 1, 5, [2, 2], shared_acc=True)
+    assert q == [[(0, 0, 0), (0, 0, 1), (0, 0, 4)], [(0, 0, 2), (0, 0, 3)]]
+    # the flag is an SHF grain only: the other mappings ignore it
+    assert (om.build_queues(om.HEAD_FIRST, 1, 2, 2, 3, [2, 1], shared_acc=True)
+            == om.build_queues(om.HEAD_FIRST, 1, 2, 2, 3, [2, 1]))
+
+
+def test_shared_acc_bijective_and_every_acc_on_every_die():
+    rng = random.Random(23)
+    for _ in range(50):
+        Hkv = rng.choice([1, 2, 4, 8])
+        Hq = Hkv * rng.choice([1, 2, 4])
+        B, nblk = rng.randint(1, 2), rng.randint(1, 40)
+        sizes = [rng.randint(1, 9) for _ in range(rng.randint(2, 3))]
+        q = om.build_queues(om.SWIZZLED_HEAD_FIRST, B, Hq, Hkv, nblk, sizes, shared_acc=True)
+        assert om.is_bijection(q, B, Hq, nblk)
+        # each die's queue stays in head-major order (a subsequence of it)
+        hm = om.head_major_tiles(B, Hq, nblk)
+        for dq in q:
+            idx = [hm.index(t) for t in dq]
+            assert idx == sorted(idx)
+        # an ACC with at least S tiles is served by every die
+        if Hq // Hkv * nblk >= sum(sizes):
+            assert all(len(ds) == len(sizes) for ds in om.acc_domains(q, Hq, Hkv).values())
+
+
+def test_shf_acc_rule_closed_form():
+    """R23's threshold by hand on B200's 126 MiB L2 (132,120,576 bytes), two
+    dies, d = 128: K+V of one head = 512*N bytes; shared iff 2*512*N > 66,060,288
+    i.e. N > 64,512 -> 32K and 64,512 per-die, 64K and 128K shared."""
+    l2 = 132120576
+    assert not om.shf_acc_shared(2, 32768, 128, l2)
+    assert not om.shf_acc_shared(2, 64512, 128, l2)
+    assert om.shf_acc_shared(2, 64513, 128, l2)
+    assert om.shf_acc_shared(2, 65536, 128, l2) and om.shf_acc_shared(2, 131072, 128, l2)
+    assert not om.shf_acc_shared(1, 131072, 128, l2)  # one die: nothing to share
+    assert not om.shf_acc_shared(2, 131072, 128, 0)   # unknown L2: the paper's grain
