@@ -17,6 +17,7 @@
 #include "../../include/attn_numa.h"
 #include "attn_bwd_sm100.cuh"
 #include "attn_fwd_sm100.cuh"
+#include "attn_fwd_pair.cuh"
 #include "attn_sched.h"
 #include "topology.cuh"
 
@@ -69,6 +70,8 @@ struct DevState {
   long long trace_cap = 0;
   bool attr_done[8] = {false, false, false, false, false, false, false, false};
   int max_clusters[4] = {0, 0, 0, 0};  // co-resident CTA-pair clusters per forward variant
+  bool pattr_done[2] = {false, false};  // attn_fwd_pair_kernel<causal>
+  int pmax_clusters[2] = {0, 0};
   // e2e host-buffer path
   void* hbuf[4] = {nullptr, nullptr, nullptr, nullptr};
   size_t hbuf_bytes[4] = {0, 0, 0, 0};
@@ -515,6 +518,52 @@ int launch_t(DevState& st, int attr_idx, const CUtensorMap& tq, const CUtensorMa
   return ATTN_OK;
 }
 
+// d in (64, 128]: one query tile per SM, the unit's two tiles on a CTA pair
+// (attn_fwd_pair.cuh) when ATTN_FWD_PAIR=1 in the environment (work in
+// progress); otherwise the two-tiles-per-CTA kernel.
+bool use_pair_kernel() {
+  static const bool on = [] {
+    const char* e = getenv("ATTN_FWD_PAIR");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+template <bool kCausal>
+int launch_pair(DevState& st, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                const KernelParams& kp, cudaStream_t s, int units) {
+  const int smem = pairk::kSmemBytes;
+  auto* fn = pairk::attn_fwd_pair_kernel<kCausal>;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const int idx = kCausal ? 1 : 0;
+  if (!st.pattr_done[idx]) {
+    ATTN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    cfg.gridDim = dim3(st.num_sms);
+    int nc = 0;
+    ATTN_CUDA(cudaOccupancyMaxActiveClusters(&nc, fn, &cfg));
+    st.pmax_clusters[idx] = nc > 0 ? nc : st.num_sms / 2;
+    st.pattr_done[idx] = true;
+  }
+  const int grid = 2 * std::min(st.pmax_clusters[idx], units);
+  cfg.gridDim = dim3(grid);
+  ATTN_CUDA(cudaLaunchKernelEx(&cfg, fn, tq, tk, tv, kp));
+  ATTN_CUDA(cudaGetLastError());
+  g_info.grid = grid;
+  g_info.block = kThreads;
+  g_info.smem_bytes = smem;
+  return ATTN_OK;
+}
+
 // Where the epilogue stores O (attn_fwd_replicated): n destinations of
 // [B][Hq_out][N][d], the shard's heads at h_off.
 struct OutSpec {
@@ -589,7 +638,11 @@ int fwd_impl(const void* q, const void* k, const void* v, void* o, int B, int Hq
 
   const int nblk = (N + kBlockM - 1) / kBlockM;  // last block may be ragged
   const int U = (nblk + 1) / 2;
-  const bool cluster = (mapping & ATTN_CLUSTER_MULTICAST) != 0;
+  // head dims > 64 run the CTA-pair kernel (attn_fwd_pair.cuh) over the plain
+  // per-unit queues whether or not ATTN_CLUSTER_MULTICAST is given (it is a
+  // CTA-pair kernel); head dims <= 64 honour the flag with the kCl = 2 path
+  const bool pair = d > 64 && use_pair_kernel();
+  const bool cluster = (mapping & ATTN_CLUSTER_MULTICAST) != 0 && !pair;
   mapping &= ~ATTN_CLUSTER_MULTICAST;
   // cluster units: with an even GQA group the pair takes the same unit of two
   // query heads of one KV group (identical K/V blocks); otherwise two adjacent
@@ -633,15 +686,20 @@ int fwd_impl(const void* q, const void* k, const void* v, void* o, int B, int Hq
 
   CUtensorMap tq, tk, tv;
   if ((rc = make_tmap(&tq, q, (long long)B * Hq, N, d, kBlockM)) != ATTN_OK) return rc;
-  // clusters: each CTA of a pair loads half the rows of every K/V block
-  const int kv_box = cluster ? kBlockN / 2 : kBlockN;
-  if ((rc = make_tmap(&tk, k, (long long)B * Hkv, N, d, kv_box)) != ATTN_OK) return rc;
-  if ((rc = make_tmap(&tv, v, (long long)B * Hkv, N, d, kv_box)) != ATTN_OK) return rc;
+  // clusters: each CTA loads half the rows of every K/V block; CTA-pair MMA
+  // (pair kernel): half the keys of K, half the head-dim columns of V
+  const int k_box = (cluster || pair) ? kBlockN / 2 : kBlockN;
+  const int v_box = cluster ? kBlockN / 2 : kBlockN;
+  if ((rc = make_tmap(&tk, k, (long long)B * Hkv, N, d, k_box)) != ATTN_OK) return rc;
+  if ((rc = make_tmap(&tv, v, (long long)B * Hkv, N, d, v_box)) != ATTN_OK) return rc;
 
   const int total = B * Hq * U;
   const int cunits = B * Hsched * Usched;
   const int grid = std::min(st.num_sms, total);
-  if (dpad == 128 && causal) rc = launch_t<128, true>(st, 0, tq, tk, tv, kp, grid, stream, cluster, cunits);
+  if (pair)
+    rc = causal ? launch_pair<true>(st, tq, tk, tv, kp, stream, total)
+                : launch_pair<false>(st, tq, tk, tv, kp, stream, total);
+  else if (dpad == 128 && causal) rc = launch_t<128, true>(st, 0, tq, tk, tv, kp, grid, stream, cluster, cunits);
   else if (dpad == 128) rc = launch_t<128, false>(st, 1, tq, tk, tv, kp, grid, stream, cluster, cunits);
   else if (causal) rc = launch_t<64, true>(st, 2, tq, tk, tv, kp, grid, stream, cluster, cunits);
   else rc = launch_t<64, false>(st, 3, tq, tk, tv, kp, grid, stream, cluster, cunits);
@@ -1111,7 +1169,7 @@ int attn_schedule_order(int B, int Hq, int Hkv, int N, int mapping, int n_domain
     queue_len[qi] = sp.q[qi].len;
     for (int pos = 0; pos < sp.q[qi].len; ++pos) {
       int b, h, u;
-      decode_unit(sp.q[qi], pos, Hq, U, b, h, u);
+      decode_unit(sp, qi, pos, Hq, U, b, h, u);
       if ((sp.descending >> qi) & 1) u = U - 1 - u;
       out[3 * w] = b;
       out[3 * w + 1] = h;

@@ -115,7 +115,7 @@ __device__ __forceinline__ void bwd_scheduler(const BwdParams& p, BCtrl* ctrl, i
       if (exhausted & (1u << qq)) continue;
       const int pos = atomicAdd(&p.counters[qq * 32], 1);
       if (pos < p.sched.q[qq].len) {
-        decode_unit(p.sched.q[qq], pos, Hsched, p.U, b, h, u);
+        decode_unit(p.sched, qq, pos, Hsched, p.U, b, h, u);
         if ((p.sched.descending >> qq) & 1) u = p.U - 1 - u;
         qi = qq;
         break;

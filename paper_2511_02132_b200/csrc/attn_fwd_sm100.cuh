@@ -264,7 +264,7 @@ __device__ __forceinline__ void run_scheduler(const KernelParams& p, CT* ctrl) {
       if (exhausted & (1u << qq)) continue;
       const int pos = atomicAdd(&p.counters[qq * 32], 1);
       if (pos < p.sched.q[qq].len) {
-        decode_unit(p.sched.q[qq], pos, p.Hsched, p.Usched, b, h, u);
+        decode_unit(p.sched, qq, pos, p.Hsched, p.Usched, b, h, u);
         if ((p.sched.descending >> qq) & 1) u = p.Usched - 1 - u;
         qi = qq;
         stolen = t > 0;

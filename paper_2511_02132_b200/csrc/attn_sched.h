@@ -17,10 +17,11 @@
 //           S:172): queue d holds the KV groups g = h_lo + i*stride
 //           (i < n_groups) in order for b, for u, for g, for the G heads of g.
 //   kind 4  interleaved head-major slots (Swizzled Head-first with the ACC
-//           shared by all dies, R23): of every `stride` consecutive
-//           units of the head-major list, queue d holds the h_cnt units at
-//           offsets [start, start + h_cnt):
-//           hm = (pos / h_cnt) * stride + start + pos % h_cnt
+//           shared by all dies, R23): the head-major list is cut
+//           into periods of S = sum(sizes) units and die d owns sizes[d]
+//           slots of every period, spread evenly (nested Bresenham: die 0
+//           takes its share of the S slots, die 1 its share of the rest, ...):
+//           hm = (pos / sizes[d]) * S + slot(d, pos % sizes[d])
 // Block-first and head-first use ONE queue popped by every SM of every die;
 // swizzled head-first uses one queue per die (reading R8).
 #pragma once
@@ -43,7 +44,7 @@ struct QueueDesc {
                // 4 interleaved head-major slots
   int start;   // first position (kinds 0, 1); kind 4: first slot of the period
   int len;     // number of units in the queue
-  int h_lo;    // kind 2: first query head; kind 3: first KV group
+  int h_lo;    // kind 2: first query head; kind 3: first KV group; kind 4: die index d
   int h_cnt;   // kind 2: query heads per batch item; kind 3: number of KV groups; kind 4: slots per period
   int stride;  // kind 3: KV-group stride (= number of dies); kind 4: period (units)
   int G;       // kind 3: query heads per KV group
@@ -55,9 +56,23 @@ struct SchedParams {
   int descending;                      // bit q set: queue q visits each head's units in descending order
   int queue_of_domain[kMaxQueues];     // die -> queue popped first
   QueueDesc q[kMaxQueues];
+  int slot_T[kMaxQueues + 1];          // kind 4: slot_T[e] = sizes[e] + ... + sizes[D-1]; slot_T[D] = 0
 };
 
-ATTN_HD void decode_unit(const QueueDesc& qd, int pos, int Hq, int U, int& b, int& h, int& u) {
+// Kind 4: period slot of the r-th unit die d owns (0 <= r < sizes[d]).  Die
+// d owns the slots i of its sub-period (the T_d slots dies 0..d-1 left) with
+// floor((i+1) a / T_d) > floor(i a / T_d), a = sizes[d]: the r-th is
+// ceil((r+1) T_d / a) - 1; the slots it leaves form the next sub-period, whose
+// k-th is slot floor(k T_d / T_(d+1)) of this one.  The last die takes the rest.
+ATTN_HD int interleave_slot(const int* T, int d, int r) {
+  const int a = T[d] - T[d + 1];
+  long long idx = (T[d + 1] == 0) ? r : ((long long)(r + 1) * T[d] + a - 1) / a - 1;
+  for (int e = d - 1; e >= 0; --e) idx = idx * T[e] / T[e + 1];
+  return (int)idx;
+}
+
+ATTN_HD void decode_unit(const SchedParams& sp, int qi, int pos, int Hq, int U, int& b, int& h, int& u) {
+  const QueueDesc& qd = sp.q[qi];
   if (qd.kind == 0) {
     const int p = qd.start + pos;
     b = p / (U * Hq);
@@ -65,7 +80,8 @@ ATTN_HD void decode_unit(const QueueDesc& qd, int pos, int Hq, int U, int& b, in
     u = r / Hq;
     h = r % Hq;
   } else if (qd.kind == 1 || qd.kind == 4) {
-    const int hm = (qd.kind == 1) ? qd.start + pos : (pos / qd.h_cnt) * qd.stride + qd.start + pos % qd.h_cnt;
+    const int hm = (qd.kind == 1) ? qd.start + pos
+                                  : (pos / qd.h_cnt) * qd.stride + interleave_slot(sp.slot_T, qd.h_lo, pos % qd.h_cnt);
     b = hm / (Hq * U);
     h = (hm / U) % Hq;
     u = hm % U;
@@ -151,18 +167,21 @@ inline bool build_queues(int mapping_arg, int B, int Hq, int Hkv, int U, int n_d
   for (int d = 0; d < D; ++d) sp.queue_of_domain[d] = d;
   if (mapping == 2 && (mapping_arg & kShfAccShared)) {
     // R23: every die takes its SM share of each period of S consecutive
-    // head-major units, so all dies serve the same ACC at the same time
-    int S = 0;
-    for (int d = 0; d < D; ++d) S += sms_per_domain[d];
+    // head-major units, spread over the period, so all dies serve the same
+    // ACC at the same time and at the same point of its causal prefix
+    sp.slot_T[D] = 0;
+    for (int d = D - 1; d >= 0; --d) {
+      if (sms_per_domain[d] < 0) return false;
+      sp.slot_T[d] = sp.slot_T[d + 1] + sms_per_domain[d];
+    }
+    const int S = sp.slot_T[0];
     if (S <= 0) return false;
-    int c = 0;
+    const int full = total / S, rem = total % S;
     for (int d = 0; d < D; ++d) {
       const int sd = sms_per_domain[d];
-      if (sd < 0) return false;
-      const int full = total / S, rem = total % S;
-      const int tail = rem > c ? (rem - c < sd ? rem - c : sd) : 0;
-      sp.q[d] = QueueDesc{4, c, full * sd + tail, 0, sd, S, 0};
-      c += sd;
+      int tail = 0;  // owned slots in the partial last period
+      for (int r = 0; r < sd; ++r) tail += interleave_slot(sp.slot_T, d, r) < rem;
+      sp.q[d] = QueueDesc{4, 0, full * sd + tail, d, sd, S, 0};
     }
     return true;
   }

@@ -34,8 +34,15 @@
     long long* cyc_out_ = reinterpret_cast<long long*>(trace) + (blockIdx.x * 8 + (warp_index)) * 8;    \
     for (int cyc_i_ = 0; cyc_i_ < 8; ++cyc_i_) cyc_out_[cyc_i_] = cyc_[cyc_i_];                          \
   }
+// pair kernel: one record of 8 counters per (CTA < 64, warp 0..11)
+#define ATTN_CYC_WRITE12(trace, warp_index)                                                                \
+  if ((trace) && (threadIdx.x & 31) == 0 && blockIdx.x < 64) {                                             \
+    long long* cyc_out_ = reinterpret_cast<long long*>(trace) + (blockIdx.x * 12 + (warp_index)) * 8;   \
+    for (int cyc_i_ = 0; cyc_i_ < 8; ++cyc_i_) cyc_out_[cyc_i_] = cyc_[cyc_i_];                          \
+  }
 #define ATTN_INSTRUMENTED 1
 #else
+#define ATTN_CYC_WRITE12(trace, warp_index)
 #define ATTN_CYC_DECL()
 #define ATTN_CYC_START()
 #define ATTN_CYC_ADD(i)

@@ -10,7 +10,7 @@ import sys
 so = sys.argv[1]
 D, causal, cl = (sys.argv[2:5] + ["128", "0", "1"][len(sys.argv[2:5]):]) if len(sys.argv) > 2 else ("128", "0", "1")
 sass = subprocess.run(["cuobjdump", "-sass", so], capture_output=True, text=True).stdout
-name = f"attn_fwd_sm100_kernelILi{D}ELb{causal}ELi{cl}E"
+name = sys.argv[5] if len(sys.argv) > 5 else f"attn_fwd_sm100_kernelILi{D}ELb{causal}ELi{cl}E"
 start = sass.index(name)
 end = sass.find("Function :", start + 10)
 lines = sass[start:end].split("\n")

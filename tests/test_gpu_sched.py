@@ -88,7 +88,7 @@ def test_shared_acc_grain_on_device():
     t = attn_topology(0)
     if t["n_domains"] < 2:
         pytest.skip("probe found one domain")
-    B, Hq, Hkv, N, d = 1, 8, 8, 16384, 128
+    B, Hq, Hkv, N, d = 1, 2, 2, 65536, 128  # 256 units per ACC: more than one period of 148
     tr, o_sh = _trace_run(B, Hq, Hkv, N, d, True, "swizzled_head_first:shared")
     _, o_pd = _trace_run(B, Hq, Hkv, N, d, True, "swizzled_head_first:per_die")
     assert torch.equal(o_sh.view(torch.int16), o_pd.view(torch.int16))
