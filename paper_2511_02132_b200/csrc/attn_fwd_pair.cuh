@@ -1,6 +1,6 @@
 // attn_fwd_pair.cuh -- head dim 65..128 forward on CTA pairs: one 128-row
 // query tile per SM, the two tiles of a work unit computed by cta_group::2
-// (M = 256) tensor-core MMAs, a 3-deep ring of S buffers in TMEM.
+// (M = 256) tensor-core MMAs, S and P double-buffered in TMEM.
 //
 // Same math, work units, queues and scheduler as attn_fwd_sm100.cuh (PAPER.md
 // eq:fa :149-155, the online-softmax fix-up :172); what changes is how the SM
@@ -9,18 +9,21 @@
 // aliases S_t, and each tile's iteration is a chain
 //     softmax_t(j) -> O_t += P_t V_j -> S_t = Q_t K_(j+1) -> softmax_t(j+1)
 // whose tensor part (1024 cycles) plus latencies leaves the tensor pipe idle
-// ~30% of the time.  Here an SM owns ONE 128-row tile:
-// TMEM = S ring [0,384) (3 x 128 columns, P_j aliased into S_(j mod 3)) and
-// O [384,512).  The MMA warp issues S(j+3) right after O += P_j V_j, so S of
-// the next two key blocks is always ready and the softmax never waits for the
-// tensor pipe.  Two softmax warpgroups take alternate key blocks (one row per
-// thread each), so two blocks' exps and row maxima overlap on every SMSP; the
-// running max m is handed from block to block through shared memory right
-// after each block's row max (so the next block's exps can start); each
-// warpgroup keeps its own partial row sum l (rescaled when m moves) and the
-// two partials are merged once per unit by the warpgroup that writes the
-// output.  The same threshold-rescale rule, P and O += P V as the
-// two-tiles-per-CTA kernel; only l's summation order differs.
+// ~30% of the time.  Here an SM owns ONE 128-row tile
+// and TMEM holds S0 S1 [0,256), P0 P1 [256,384) (bf16 pairs, 64 columns
+// each) and O [384,512).  Block g of the CTA (counted over all its units)
+// uses S_(g%2) and P_(g%2) and is the softmax work of warpgroup g%2, so each
+// softmax warpgroup owns one S and one P buffer.  P does not alias S, so the
+// MMA warp issues S(g+2) into S_(g%2) as soon as that warpgroup has LOADED
+// S(g) into registers, long before O += P(g) V(g): the tensor pipe never
+// waits for a softmax to finish before the next S, and a warpgroup finds
+// S(g+2) ready when it comes back.  Two blocks' exps and row maxima overlap
+// on every SMSP; the running max m is handed from block to block through
+// shared memory right after each block's row max (so the next block's exps
+// can start); each warpgroup keeps its own partial row sum l (rescaled when
+// m moves) and the two partials are merged once per unit by the warpgroup
+// that writes the output.  The same threshold-rescale rule, P and O += P V
+// as the two-tiles-per-CTA kernel; only l's summation order differs.
 //
 // One tile per SM alone would need 160 KB of SMEM traffic per 1024 tensor
 // cycles (Q and K read by S, V by O += P V, K and V written by TMA: more than
@@ -36,12 +39,14 @@
 // mapping's queues (the plain per-unit queues: B * Hq * U entries).
 //
 // CTA layout (384 threads, one CTA per SM, persistent; clusters of 2):
-//   warp 0      TMA producer: own Q tile; own halves of K/V, ring order
-//               K0 K1 K2 V0 K3 V1 K4 ... (K three blocks ahead of V)
-//   warp 1      MMA issuer (leader CTA): S(0..2), then per block
-//               O += P_j V_j, S(j+3); idle in the peer CTA
+//   warp 0      TMA producer: own Q tile; own halves of K and V into a K
+//               ring and a V ring, in the order K0 K1 K2 V0 K3 V1 ...
+//   warp 1      S issuer (leader CTA): S(g) into S_(g%2) as soon as K(g) has
+//               landed and block g-2 has left the buffer; idle in the peer
 //   warp 2      TMEM allocator (both CTAs) + (leader) work scheduler
-//   warp 3      idle
+//   warp 3      O += P V issuer (leader CTA): O += P(g) V(g) as soon as both
+//               SMs published P(g); idle in the peer.  Two issuers, so an S
+//               never queues behind an O += P V that waits for a softmax
 //   warps 4-7   softmax + fix-up (+ epilogue) of the even key blocks
 //   warps 8-11  the same for the odd key blocks (block parity counted over
 //               all the CTA's blocks; the warpgroup of a unit's last block
@@ -53,15 +58,14 @@ namespace attn {
 namespace pairk {
 
 constexpr int D = 128;
-constexpr int kSSlots = 3;
+constexpr int kColP = 256;  // TMEM column of P0 (P1 at +64)
 constexpr int kColO = 384;  // TMEM column of O
-#ifndef ATTN_PAIR_KV_SLOTS
-#define ATTN_PAIR_KV_SLOTS 10  // half-block slots: 5 key blocks of K and V in flight
+#ifndef ATTN_PAIR_RING
+#define ATTN_PAIR_RING 5  // half-block slots per ring (K ring, V ring)
 #endif
-constexpr int kSlots = ATTN_PAIR_KV_SLOTS;
-#ifndef ATTN_PAIR_WGS
-#define ATTN_PAIR_WGS 2  // softmax warpgroups taking alternate key blocks (1: warps 8-11 idle)
-#endif
+constexpr int kRing = ATTN_PAIR_RING;
+constexpr int kSlots = 2 * kRing;
+#define ATTN_PAIR_WGS 2  // softmax warpgroups taking alternate key blocks, one S and one P buffer each
 #ifndef ATTN_PAIR_UNIT_SYNC
 #define ATTN_PAIR_UNIT_SYNC 1  // both warpgroups meet after every unit
 #endif
@@ -73,17 +77,18 @@ constexpr int kOffCtrl = kOffKV + kSlots * kHalfBytes;
 constexpr int kOffRows = kOffCtrl + 512;
 constexpr int kSmemBytes = kOffRows + 3072 + 1024;  // control block + row state + alignment slack
 static_assert(kSmemBytes <= 232448, "shared memory exceeds 227 KB");
-static_assert(kSlots <= 12, "K/V ring deeper than the barrier arrays");
+static_assert(kSlots <= 12, "K/V rings deeper than the barrier arrays");
 
 struct __align__(16) Ctrl {
   uint64_t sched_full[kSchedRing];
   uint64_t sched_empty[kSchedRing];
   uint64_t q_full, q_empty;     // q_full: leader's, both Q halves (tx); q_empty: each CTA
-  uint64_t kv_full[12];         // leader's: both SMs' halves of a slot landed (tx)
+  uint64_t kv_full[12];         // leader's: both SMs' halves of a slot landed (tx); K ring, then V ring
   uint64_t kv_empty[12];        // each CTA: the pair's MMAs are done with the slot
-  uint64_t s_full[kSSlots];     // each CTA: S_j in slot j % 3
-  uint64_t p_full[kSSlots][2];  // leader's: half h of P_j published by both SMs (8 warps)
-  uint64_t pv_done[2];          // each CTA: O += P V of the pair's g-th block done (g & 1)
+  uint64_t s_full[2];           // each CTA: S(g) in S_(g%2)
+  uint64_t s_free[2];           // leader's: both SMs' warpgroup g%2 have S(g) in registers (8 warps)
+  uint64_t p_full[2][2];        // leader's: half h of P(g) in P_(g%2), both SMs (8 warps)
+  uint64_t pv_done[4];          // each CTA: O += P V of block g done, [g & 3]
   uint64_t o_full;              // each CTA: the unit's last O += P V done
   uint64_t o_empty;             // leader's: both SMs' epilogues have read O
   uint64_t m_ready[2];          // softmax -> softmax: m after the CTA's g-th block in mrow[g & 1]
@@ -124,8 +129,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < kSchedRing; ++i) {
       ptx::mbar_init(&ctrl->sched_full[i], 1);
-      // both producers, the leader's MMA warp, both CTAs' softmax warps
-      ptx::mbar_init(&ctrl->sched_empty[i], 2 + 1 + 2 * 4 * ATTN_PAIR_WGS);
+      // both producers, the leader's two MMA issuers, both CTAs' softmax warps
+      ptx::mbar_init(&ctrl->sched_empty[i], 2 + 2 + 2 * 4 * ATTN_PAIR_WGS);
     }
     ptx::mbar_init(&ctrl->q_full, 1);
     ptx::mbar_init(&ctrl->q_empty, 1);
@@ -133,12 +138,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(&ctrl->kv_full[i], 1);
       ptx::mbar_init(&ctrl->kv_empty[i], 1);
     }
-    for (int s = 0; s < kSSlots; ++s) {
+    for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&ctrl->s_full[s], 1);
+      ptx::mbar_init(&ctrl->s_free[s], 2 * 4);
       for (int h = 0; h < 2; ++h) ptx::mbar_init(&ctrl->p_full[s][h], 2 * 4);
     }
+    for (int i = 0; i < 4; ++i) ptx::mbar_init(&ctrl->pv_done[i], 1);
     for (int i = 0; i < 2; ++i) {
-      ptx::mbar_init(&ctrl->pv_done[i], 1);
       ptx::mbar_init(&ctrl->m_ready[i], 4);
       ptx::mbar_init(&ctrl->lpart_ready[i], 4);
     }
@@ -160,6 +166,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   ptx::cluster_sync();  // peer barriers initialised before any remote arrive / TMA signal
   ptx::tc_fence_after();
 
+  // ring position -> (slot, parity) of the K ring (which = 0) or the V ring
+  struct Ring {
+    int stage = 0;
+    uint32_t phase = 0;
+    __device__ __forceinline__ void advance() {
+      if (++stage == kRing) { stage = 0; phase ^= 1; }
+    }
+  };
+
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (ATTN_SETMAXNREG) ptx::setmaxnreg_dec<kOtherRegs>();
@@ -169,22 +184,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_kv = ptx::policy_evict_normal();
       const uint32_t lead_q_full = ptx::mapa_shared(ptx::smem_u32(&ctrl->q_full), 0);
       uint32_t q_phase = 0;
-      int kv_stage = 0;
-      uint32_t kv_phase = 0;
+      Ring rk, rv;
       int seq = 0;
+      ATTN_CYC_DECL()
       // this SM's half of block j of K (which = 0: keys 64r..64r+63, all 128
       // columns, two 8 KB swizzle-atom columns) or V (which = 1: all 128 keys,
       // columns 64r..64r+63, one 16 KB atom column); the leader's kv_full
       // counts both SMs' bytes
-      ATTN_CYC_DECL()
       auto load_kv = [&](int j, int which, int kvbh) {
+        Ring& rr = which ? rv : rk;
+        const int slot = which * kRing + rr.stage;
         ATTN_CYC_START();
-        ptx::mbar_wait(&ctrl->kv_empty[kv_stage], kv_phase ^ 1);
+        ptx::mbar_wait(&ctrl->kv_empty[slot], rr.phase ^ 1);
         ATTN_CYC_ADD(0);
         ATTN_CYC_COUNT(7);
-        if (crank == 0) ptx::mbar_arrive_expect_tx(&ctrl->kv_full[kv_stage], 2 * kHalfBytes);
-        const uint32_t full = ptx::mapa_shared(ptx::smem_u32(&ctrl->kv_full[kv_stage]), 0);
-        uint8_t* dst = kv_smem + kv_stage * kHalfBytes;
+        if (crank == 0) ptx::mbar_arrive_expect_tx(&ctrl->kv_full[slot], 2 * kHalfBytes);
+        const uint32_t full = ptx::mapa_shared(ptx::smem_u32(&ctrl->kv_full[slot]), 0);
+        uint8_t* dst = kv_smem + slot * kHalfBytes;
         if (which == 0) {
 #pragma unroll
           for (int c = 0; c < D / 64; ++c)
@@ -193,7 +209,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else {
           ptx::tma_load_3d_2sm(dst, &tm_v, full, (int)crank * 64, j * kBlockN, kvbh, pol_kv);
         }
-        if (++kv_stage == kSlots) { kv_stage = 0; kv_phase ^= 1; }
+        rr.advance();
       };
       while (true) {
         const int4 e = sr.next(ctrl, true);
@@ -226,128 +242,130 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::tma_load_3d_2sm(q_smem + c * kBlockM * 128, &tm_q, lead_q_full, c * 64, qb * kBlockM, b * p.Hq + h,
                                pol_q);
         const int kvbh = b * p.Hkv + h / p.G;
-        // ring order = the MMA warp's consumption order: K0 K1 K2, then V(j) K(j+3)
-        for (int j = 0; j < min(kSSlots, n); ++j) load_kv(j, 0, kvbh);
+        // K runs two blocks ahead of V (the order the two issuers need them)
+        for (int j = 0; j < min(2, n); ++j) load_kv(j, 0, kvbh);
         for (int j = 0; j < n; ++j) {
+          if (j + 2 < n) load_kv(j + 2, 0, kvbh);
           load_kv(j, 1, kvbh);
-          if (j + kSSlots < n) load_kv(j + kSSlots, 0, kvbh);
         }
       }
       // drain: every slot's last fill released by the leader's commits, so no
       // multicast arrive is still in flight towards this CTA when it exits
-      for (int i = 0; i < kSlots; ++i) {
-        ptx::mbar_wait(&ctrl->kv_empty[kv_stage], kv_phase ^ 1);
-        if (++kv_stage == kSlots) { kv_stage = 0; kv_phase ^= 1; }
+      for (int i = 0; i < kRing; ++i) {
+        ptx::mbar_wait(&ctrl->kv_empty[rk.stage], rk.phase ^ 1);
+        ptx::mbar_wait(&ctrl->kv_empty[kRing + rv.stage], rv.phase ^ 1);
+        rk.advance();
+        rv.advance();
       }
       ATTN_CYC_WRITE12(p.trace, 0)
     }
-  } else if (warp == 1) {
-    // -------------------------------------------------------------- MMA issuer
+  } else if (warp == 1 || warp == 3) {
+    // ------------------------------------------------------- MMA issuers (leader)
     if (ATTN_SETMAXNREG) ptx::setmaxnreg_dec<kOtherRegs>();
     if (crank == 0) {
-    const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(&ctrl->tmem_base);
-    SchedReader<2, Ctrl> sr;
-    constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(2 * kBlockM, kBlockN, 0, 0);
-    constexpr uint32_t idesc_o = ptx::idesc_bf16_f32(2 * kBlockM, D, 0, 1);
-    const uint64_t dq = ptx::smem_desc_sw128(ptx::smem_u32(q_smem), 16, 1024);
-    const uint64_t dkv0 = ptx::smem_desc_sw128(ptx::smem_u32(kv_smem), 16, 1024);
-    const uint64_t dv0 = ptx::smem_desc_sw128(ptx::smem_u32(kv_smem), kBlockN * 128, 1024);
-    uint32_t q_phase = 0, p_phase = 0;  // p_phase: bit s = parity of slot s's next P
-    int kv_stage = 0;
-    uint32_t kv_phase = 0;
-    uint32_t gblk = 0;        // the pair's O += P V count over all units (pv_done[gblk & 1])
-    uint32_t units_done = 0;  // units whose epilogue frees O (o_empty phases)
-
-    // S_slot = Q K^T over 128 keys: M = 256 (both SMs' Q), N = 128 (keys
-    // 0-63 from the leader's half slot, 64-127 from the peer's)
-    auto issue_s = [&](int slot, int kslot) {
-      const uint64_t dk = dkv0 + (uint64_t)((kslot * kHalfBytes) >> 4);
-      const uint32_t d_tmem = tmem + 128u * slot;
-#pragma unroll
-      for (int k = 0; k < D / 16; ++k) {
-        const uint32_t oq = ((k >> 2) * (kBlockM * 128) + (k & 3) * 32) >> 4;
-        const uint32_t ok = ((k >> 2) * (kBlockN / 2 * 128) + (k & 3) * 32) >> 4;
-        ptx::mma_ss_2(d_tmem, dq + oq, dk + ok, idesc_s, k > 0 ? 1u : 0u);
-      }
-    };
-    // O (+)= P_slot V over the 64 keys of half h: A = P from each SM's TMEM,
-    // B = V with its 128 head-dim columns split between the SMs
-    auto issue_pv_half = [&](int slot, int vslot, bool acc, int h) {
-      const uint64_t dv = dv0 + (uint64_t)((vslot * kHalfBytes) >> 4);
-      const uint32_t a_tmem = tmem + 128u * slot;
-#pragma unroll
-      for (int k = h * 4; k < (h + 1) * 4; ++k)
-        ptx::mma_ts_2(tmem + kColO, a_tmem + k * 8, dv + (uint64_t)((k * 16 * 128) >> 4), idesc_o,
-                      (acc || k > 0) ? 1u : 0u);
-    };
-    ATTN_CYC_DECL()
-    auto take_slot = [&]() {
-      const int s = kv_stage;
-      ptx::mbar_wait(&ctrl->kv_full[s], kv_phase);
-      if (++kv_stage == kSlots) { kv_stage = 0; kv_phase ^= 1; }
-      return s;
-    };
-    // S(j) into slot j % 3; release K(j) to both SMs once it has been read
-    auto s_step = [&](int j, int n) {
-      ATTN_CYC_START();
-      const int sk = take_slot();
-      ATTN_CYC_ADD(3);
-      ptx::tc_fence_after();
-      if (ptx::elect_one_sync()) {
-        issue_s(j % kSSlots, sk);
-        ptx::mma_commit_2mc(&ctrl->s_full[j % kSSlots], kMask);
-        if (j == n - 1) ptx::mma_commit_2mc(&ctrl->q_empty, kMask);  // last read of this Q pair
-        ptx::mma_commit_2mc(&ctrl->kv_empty[sk], kMask);
-      }
-      __syncwarp();
-      ATTN_CYC_ADD(4);
-    };
-
-    while (true) {
-      const int4 e = sr.next(ctrl, false);
-      __syncwarp();
-      if (lane == 0) sr.release_prev(ctrl);
-      if (!e.w) break;
-      const int u = e.z;
-      const int n = max(tile_blocks<kCausal>(2 * u, p.nblk), tile_blocks<kCausal>(2 * u + 1, p.nblk));
-      ATTN_CYC_START();
-      ptx::mbar_wait(&ctrl->q_full, q_phase);
-      ATTN_CYC_ADD(6);
-      q_phase ^= 1;
-      for (int j = 0; j < min(kSSlots, n); ++j) s_step(j, n);
-      for (int j = 0; j < n; ++j) {
-        ATTN_CYC_START();
-        const int sv = take_slot();
-        ATTN_CYC_ADD(0);
-        const int slot = j % kSSlots;
-        const uint32_t ph = (p_phase >> slot) & 1u;
-        if (j == 0 && units_done > 0)  // O of the previous unit read by both SMs' epilogues
-          ptx::mbar_wait_cluster(&ctrl->o_empty, (units_done - 1) & 1);
-        ATTN_CYC_ADD(5);
-        ATTN_CYC_COUNT(7);
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          ATTN_CYC_START();
-          ptx::mbar_wait_cluster(&ctrl->p_full[slot][h], ph);
-          ATTN_CYC_ADD(1);
-          ptx::tc_fence_after();
-          if (ptx::elect_one_sync()) issue_pv_half(slot, sv, j > 0, h);
+      const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(&ctrl->tmem_base);
+      SchedReader<2, Ctrl> sr;
+      Ring rr;
+      uint32_t gb = 0;  // the pair's key blocks over all units
+      ATTN_CYC_DECL()
+      auto take = [&]() {
+        const int slot = (warp == 1 ? 0 : kRing) + rr.stage;
+        ptx::mbar_wait(&ctrl->kv_full[slot], rr.phase);
+        rr.advance();
+        return slot;
+      };
+      if (warp == 1) {
+        // S(g) = Q K(g)^T into S_(g%2): M = 256 (both SMs' Q), N = 128 (keys
+        // 0-63 from the leader's half slot, 64-127 from the peer's)
+        constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(2 * kBlockM, kBlockN, 0, 0);
+        const uint64_t dq = ptx::smem_desc_sw128(ptx::smem_u32(q_smem), 16, 1024);
+        const uint64_t dkv0 = ptx::smem_desc_sw128(ptx::smem_u32(kv_smem), 16, 1024);
+        uint32_t q_phase = 0;
+        while (true) {
+          const int4 e = sr.next(ctrl, false);
           __syncwarp();
-          ATTN_CYC_ADD(2);
+          if (lane == 0) sr.release_prev(ctrl);
+          if (!e.w) break;
+          const int u = e.z;
+          const int n = max(tile_blocks<kCausal>(2 * u, p.nblk), tile_blocks<kCausal>(2 * u + 1, p.nblk));
+          ptx::mbar_wait(&ctrl->q_full, q_phase);
+          q_phase ^= 1;
+          for (int j = 0; j < n; ++j, ++gb) {
+            ATTN_CYC_START();
+            // S_(g%2) free once both SMs' warpgroup g%2 loaded S(g-2)
+            if (gb >= 2) ptx::mbar_wait_cluster(&ctrl->s_free[gb & 1], ((gb >> 1) - 1) & 1);
+            ATTN_CYC_ADD(3);
+            const int sk = take();
+            ATTN_CYC_ADD(0);
+            ATTN_CYC_COUNT(7);
+            ptx::tc_fence_after();
+            if (ptx::elect_one_sync()) {
+              const uint64_t dk = dkv0 + (uint64_t)((sk * kHalfBytes) >> 4);
+              const uint32_t d_tmem = tmem + 128u * (gb & 1);
+#pragma unroll
+              for (int k = 0; k < D / 16; ++k) {
+                const uint32_t oq = ((k >> 2) * (kBlockM * 128) + (k & 3) * 32) >> 4;
+                const uint32_t ok = ((k >> 2) * (kBlockN / 2 * 128) + (k & 3) * 32) >> 4;
+                ptx::mma_ss_2(d_tmem, dq + oq, dk + ok, idesc_s, k > 0 ? 1u : 0u);
+              }
+              ptx::mma_commit_2mc(&ctrl->s_full[gb & 1], kMask);
+              if (j == n - 1) ptx::mma_commit_2mc(&ctrl->q_empty, kMask);  // last read of this Q pair
+              ptx::mma_commit_2mc(&ctrl->kv_empty[sk], kMask);
+            }
+            __syncwarp();
+            ATTN_CYC_ADD(4);
+          }
         }
-        p_phase ^= 1u << slot;
-        if (ptx::elect_one_sync()) {
-          ptx::mma_commit_2mc(&ctrl->pv_done[gblk & 1], kMask);
-          if (j == n - 1) ptx::mma_commit_2mc(&ctrl->o_full, kMask);
-          ptx::mma_commit_2mc(&ctrl->kv_empty[sv], kMask);
+        ATTN_CYC_WRITE12(p.trace, 1)
+      } else {
+        // O (+)= P(g) V(g): A = P_(g%2) from each SM's TMEM, B = V with its
+        // 128 head-dim columns split between the SMs; P published in halves
+        constexpr uint32_t idesc_o = ptx::idesc_bf16_f32(2 * kBlockM, D, 0, 1);
+        const uint64_t dv0 = ptx::smem_desc_sw128(ptx::smem_u32(kv_smem), kBlockN * 128, 1024);
+        uint32_t units_done = 0;  // units whose epilogue frees O (o_empty phases)
+        while (true) {
+          const int4 e = sr.next(ctrl, false);
+          __syncwarp();
+          if (lane == 0) sr.release_prev(ctrl);
+          if (!e.w) break;
+          const int u = e.z;
+          const int n = max(tile_blocks<kCausal>(2 * u, p.nblk), tile_blocks<kCausal>(2 * u + 1, p.nblk));
+          for (int j = 0; j < n; ++j, ++gb) {
+            ATTN_CYC_START();
+            const int sv = take();
+            ATTN_CYC_ADD(0);
+            if (j == 0 && units_done > 0)  // O of the previous unit read by both SMs' epilogues
+              ptx::mbar_wait_cluster(&ctrl->o_empty, (units_done - 1) & 1);
+            ATTN_CYC_ADD(5);
+            ATTN_CYC_COUNT(7);
+            const uint64_t dv = dv0 + (uint64_t)((sv * kHalfBytes) >> 4);
+            const uint32_t a_tmem = tmem + kColP + 64u * (gb & 1);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              ATTN_CYC_START();
+              ptx::mbar_wait_cluster(&ctrl->p_full[gb & 1][h], (gb >> 1) & 1);
+              ATTN_CYC_ADD(1);
+              ptx::tc_fence_after();
+              if (ptx::elect_one_sync()) {
+#pragma unroll
+                for (int k = h * 4; k < (h + 1) * 4; ++k)
+                  ptx::mma_ts_2(tmem + kColO, a_tmem + k * 8, dv + (uint64_t)((k * 16 * 128) >> 4), idesc_o,
+                                (j > 0 || k > 0) ? 1u : 0u);
+              }
+              __syncwarp();
+              ATTN_CYC_ADD(2);
+            }
+            if (ptx::elect_one_sync()) {
+              ptx::mma_commit_2mc(&ctrl->pv_done[gb & 3], kMask);
+              if (j == n - 1) ptx::mma_commit_2mc(&ctrl->o_full, kMask);
+              ptx::mma_commit_2mc(&ctrl->kv_empty[sv], kMask);
+            }
+            __syncwarp();
+          }
+          ++units_done;
         }
-        __syncwarp();
-        ++gblk;
-        if (j + kSSlots < n) s_step(j + kSSlots, n);
+        ATTN_CYC_WRITE12(p.trace, 3)
       }
-      ++units_done;
-    }
-    ATTN_CYC_WRITE12(p.trace, 1)
     }
   } else if (warp == 2) {
     // --------------------------------------------------------------- scheduler
@@ -363,7 +381,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
     const float c = p.scale_log2;
     SchedReader<2, Ctrl> sr;
-    uint32_t s_phase = 0, o_phase = 0;  // s_phase: bit s = parity of slot s's next S
+    uint32_t o_phase = 0;
     uint32_t g = 0;                     // the CTA's blocks over all units (both warpgroups count all)
     uint32_t un = 0;                    // units with two or more blocks so far (lpart hand-overs)
     float l_w = 0.f, m_w = -INFINITY;   // this warpgroup's partial row sum and the max it is relative to
@@ -382,17 +400,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int last_blk = p.nblk - 1;
       const int tail_lim = p.N - last_blk * kBlockN - 1;  // last block: local key k visible iff k <= tail_lim
       for (int j = 0; j < n; ++j, ++g) {
-        const int slot = j % kSSlots;
-        const uint32_t sph = (s_phase >> slot) & 1u;
-        s_phase ^= 1u << slot;
-        if ((g & (ATTN_PAIR_WGS - 1u)) != wg) continue;  // the other warpgroup's block
+        if ((g & 1u) != wg) continue;  // the other warpgroup's block
         ATTN_CYC_START();
-        ptx::mbar_wait(&ctrl->s_full[slot], sph);
+        ptx::mbar_wait(&ctrl->s_full[wg], (g >> 1) & 1);
         ATTN_CYC_ADD(0);
         ATTN_CYC_COUNT(7);
         ptx::tc_fence_after();
         uint32_t r[kBlockN];
-        ptx::tmem_ld128(trow + 128u * slot, r);
+        ptx::tmem_ld128(trow + 128u * wg, r);
+        // S(g) is in registers: the MMA warp may compute S(g+2) into S_wg
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster_relaxed(ptx::mapa_shared(ptx::smem_u32(&ctrl->s_free[wg]), 0));
         // visible local keys are k <= lim: causal diagonal block (key <= query)
         // and/or the ragged last key block (key < N)
         int lim = kBlockN;
@@ -440,11 +459,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) ptx::mbar_arrive(&ctrl->m_ready[g & 1]);
         if (__any_sync(0xffffffffu, rescale)) {
           // fix-up: O *= exp2((m_old - m_new) c) once O += P V
-          // of the previous block is complete.  pv_done[(g-1) & 1] has
-          // completed (g-1) >> 1 or (g-1) >> 1 + 1 phases: S_j landing implies
-          // every earlier block but the last two is done, and P_j is not out.
+          // of the previous block is complete.  pv_done[(g-1) & 3] has
+          // completed (g-1) >> 2 or (g-1) >> 2 + 1 phases: block g-5 is done
+          // (the other warpgroup waited for it before storing P(g-3), and it
+          // published m(g-1) after that), and P(g) is not out yet.
           const uint32_t g1 = g - 1;
-          ptx::mbar_wait(&ctrl->pv_done[g1 & 1], (g1 >> 1) & 1);
+          ptx::mbar_wait(&ctrl->pv_done[g1 & 3], (g1 >> 2) & 1);
           ptx::tc_fence_after();
 #pragma unroll
           for (int cc = 0; cc < D; cc += 32) {
@@ -485,14 +505,21 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef ATTN_CYCLES_EXP
             ATTN_CYC_ADD(3);
 #endif
-            ptx::tmem_st32(trow + 128u * slot + h * 32, r + h * 32);
+            if (h == 0 && g >= 2) {
+              // P_wg is free once O += P(g-2) V is done (pv_done[(g-2) & 3]:
+              // block g-6 is done, this warpgroup waited for it before P(g-4))
+              const uint32_t g2 = g - 2;
+              ptx::mbar_wait(&ctrl->pv_done[g2 & 3], (g2 >> 2) & 1);
+              ptx::tc_fence_after();
+            }
+            ptx::tmem_st32(trow + kColP + 64u * wg + h * 32, r + h * 32);
             ptx::tmem_wait_st();
 #ifdef ATTN_CYCLES_EXP
             ATTN_CYC_ADD(5);
 #endif
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive_cluster_relaxed(ptx::mapa_shared(ptx::smem_u32(&ctrl->p_full[slot][h]), 0));
+            if (lane == 0) ptx::mbar_arrive_cluster_relaxed(ptx::mapa_shared(ptx::smem_u32(&ctrl->p_full[wg][h]), 0));
 #ifdef ATTN_CYCLES_EXP
             ATTN_CYC_ADD(6);
 #endif
@@ -572,8 +599,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (ATTN_PAIR_UNIT_SYNC) ptx::named_bar_sync(1, 32 * 4 * ATTN_PAIR_WGS);
     }
     ATTN_CYC_WRITE12(p.trace, warp)
-  } else {
-    if (ATTN_SETMAXNREG) ptx::setmaxnreg_dec<kOtherRegs>();  // warp 3: idle
   }
 
   ptx::tc_fence_before();

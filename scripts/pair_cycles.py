@@ -41,9 +41,10 @@ def show(title, rec, names):
 
 show("producer (leader)", lead[:, 0], ["kv_empty wait", "", "q_empty wait (per event)"])
 show("producer (peer)", peer[:, 0], ["kv_empty wait", "", "q_empty wait (per event)"])
-show("MMA (leader), per key block", lead[:, 1],
-     ["V kv_full wait", "p_full wait", "PV issue", "K kv_full wait", "S issue+commits", "o_empty wait",
-      "q_full wait"])
+show("S issuer (leader), per key block", lead[:, 1],
+     ["K kv_full wait", "", "", "s_free wait", "S issue+commits", "", ""])
+show("PV issuer (leader), per key block", lead[:, 3],
+     ["V kv_full wait", "p_full wait", "PV issue", "", "", "o_empty wait", ""])
 sm = np.concatenate([c[:, w] for w in range(4, 12)])
 show("softmax warps, per own block", sm,
      ["S wait", "ld+mask+max", "m wait", "exps+P (+fixup)", "l wait", "epilogue", "o_full wait"] if len(sys.argv) < 8 else
