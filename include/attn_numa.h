@@ -114,10 +114,10 @@ typedef enum {
  * dies share ONE L2 (lines homed by address; the probe measures that a far
  * line is not replicated near, far_lines_cached_near = 0), so serving one ACC
  * per die keeps n_domains ACC K/V footprints live in that L2 at once.
- *   ATTN_SHF_ACC_SHARED   every ACC is served by all dies together: of every
- *                         S = sum(sms_per_domain) consecutive units of the
- *                         head-major order, die d's queue takes its
- *                         sms_per_domain[d] units (per-die queues, stealing);
+ *   ATTN_SHF_ACC_SHARED   every ACC is served by all dies together: the dies
+ *                         form ONE capacity domain, and swizzled head-first
+ *                         over one domain is the head-major order (one queue
+ *                         popped by every SM);
  *   ATTN_SHF_ACC_PER_DIE  the paper's literal grain (one die per ACC) always;
  *   neither               the library decides per call with
  *                         attn_shf_acc_shared(n_domains, N, d, l2_bytes).

@@ -157,9 +157,9 @@ def build_queues(mapping: str, B: int, Hq: int, Hkv: int, nblk: int,
     (the B200 analogue of round-robin dispatch: consecutive tiles of a head
     land on SMs of both dies).  swizzled_head_first: one queue per die
     (R8), each die serving its ACCs one at a time in head-major order; with
-    shared_acc (R23) all dies serve the same ACC: of every S = sum(sizes)
-    consecutive tiles of the head-major list, die d takes sizes[d] of them
-    (the ones after the first sizes[0] + ... + sizes[d-1]).
+    shared_acc (R23) all dies serve the same ACC: they form one capacity
+    domain, and swizzled head-first over one domain is head-first (S:189,
+    S:206).
     """
     if mapping == BLOCK_FIRST:
         return [block_major_tiles(B, Hq, nblk)]
@@ -187,14 +187,7 @@ def build_queues(mapping: str, B: int, Hq: int, Hkv: int, nblk: int,
         return [head_major_tiles(B, Hq, nblk)]
     queues: List[List[Tile]] = [[] for _ in range(D)]
     if shared_acc:
-        S = sum(domain_sizes)
-        first_slot = [sum(domain_sizes[:e]) for e in range(D)]
-        for p, tile in enumerate(head_major_tiles(B, Hq, nblk)):
-            slot = p % S
-            for d in range(D):
-                if first_slot[d] <= slot < first_slot[d] + domain_sizes[d]:
-                    queues[d].append(tile)
-        return queues
+        return [head_major_tiles(B, Hq, nblk)]
     if Hkv >= D:
         # Fig. 7 generalised: per batch item, ACCs [cut_d, cut_{d+1}) -> die d.
         cuts = _prop_cuts(Hkv, domain_sizes)

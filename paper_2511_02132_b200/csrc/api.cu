@@ -707,7 +707,7 @@ int fwd_impl(const void* q, const void* k, const void* v, void* o, int B, int Hq
   g_info.units = total;
   g_info.n_queues = kp.sched.n_queues;
   g_info.shf_acc_shared = ((mapping & kMapMask) == ATTN_MAP_SWIZZLED_HEAD_FIRST && (mapping & kShfAccShared) &&
-                           kp.sched.n_queues > 1) ? 1 : 0;
+                           st.active.n_domains > 1) ? 1 : 0;
   g_info.kernel_launches = 1;
   return ATTN_OK;
 }

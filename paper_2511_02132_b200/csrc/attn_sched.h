@@ -16,14 +16,10 @@
 //   kind 3  strided groups, block-major (Swizzled Block-first, P:236-243,
 //           S:172): queue d holds the KV groups g = h_lo + i*stride
 //           (i < n_groups) in order for b, for u, for g, for the G heads of g.
-//   kind 4  interleaved head-major slots (Swizzled Head-first with the ACC
-//           shared by all dies, R23): the head-major list is cut
-//           into periods of S = sum(sizes) units and die d owns sizes[d]
-//           slots of every period, spread evenly (nested Bresenham: die 0
-//           takes its share of the S slots, die 1 its share of the rest, ...):
-//           hm = (pos / sizes[d]) * S + slot(d, pos % sizes[d])
 // Block-first and head-first use ONE queue popped by every SM of every die;
-// swizzled head-first uses one queue per die (reading R8).
+// swizzled head-first uses one queue per die (reading R8), or, when
+// its ACCs are shared by all dies (R23), the one head-major queue of a single
+// capacity domain.
 #pragma once
 #include <cstdint>
 
@@ -40,13 +36,12 @@ namespace attn {
 constexpr int kMaxQueues = 8;
 
 struct QueueDesc {
-  int kind;    // 0 block-major range, 1 head-major range, 2 per-batch head range, 3 strided groups,
-               // 4 interleaved head-major slots
-  int start;   // first position (kinds 0, 1); kind 4: first slot of the period
+  int kind;    // 0 block-major range, 1 head-major range, 2 per-batch head range, 3 strided groups
+  int start;   // first position (kinds 0, 1)
   int len;     // number of units in the queue
-  int h_lo;    // kind 2: first query head; kind 3: first KV group; kind 4: die index d
-  int h_cnt;   // kind 2: query heads per batch item; kind 3: number of KV groups; kind 4: slots per period
-  int stride;  // kind 3: KV-group stride (= number of dies); kind 4: period (units)
+  int h_lo;    // kind 2: first query head; kind 3: first KV group
+  int h_cnt;   // kind 2: query heads per batch item; kind 3: number of KV groups
+  int stride;  // kind 3: KV-group stride (= number of dies)
   int G;       // kind 3: query heads per KV group
 };
 
@@ -56,20 +51,7 @@ struct SchedParams {
   int descending;                      // bit q set: queue q visits each head's units in descending order
   int queue_of_domain[kMaxQueues];     // die -> queue popped first
   QueueDesc q[kMaxQueues];
-  int slot_T[kMaxQueues + 1];          // kind 4: slot_T[e] = sizes[e] + ... + sizes[D-1]; slot_T[D] = 0
 };
-
-// Kind 4: period slot of the r-th unit die d owns (0 <= r < sizes[d]).  Die
-// d owns the slots i of its sub-period (the T_d slots dies 0..d-1 left) with
-// floor((i+1) a / T_d) > floor(i a / T_d), a = sizes[d]: the r-th is
-// ceil((r+1) T_d / a) - 1; the slots it leaves form the next sub-period, whose
-// k-th is slot floor(k T_d / T_(d+1)) of this one.  The last die takes the rest.
-ATTN_HD int interleave_slot(const int* T, int d, int r) {
-  const int a = T[d] - T[d + 1];
-  long long idx = (T[d + 1] == 0) ? r : ((long long)(r + 1) * T[d] + a - 1) / a - 1;
-  for (int e = d - 1; e >= 0; --e) idx = idx * T[e] / T[e + 1];
-  return (int)idx;
-}
 
 ATTN_HD void decode_unit(const SchedParams& sp, int qi, int pos, int Hq, int U, int& b, int& h, int& u) {
   const QueueDesc& qd = sp.q[qi];
@@ -79,9 +61,8 @@ ATTN_HD void decode_unit(const SchedParams& sp, int qi, int pos, int Hq, int U, 
     const int r = p % (U * Hq);
     u = r / Hq;
     h = r % Hq;
-  } else if (qd.kind == 1 || qd.kind == 4) {
-    const int hm = (qd.kind == 1) ? qd.start + pos
-                                  : (pos / qd.h_cnt) * qd.stride + interleave_slot(sp.slot_T, qd.h_lo, pos % qd.h_cnt);
+  } else if (qd.kind == 1) {
+    const int hm = qd.start + pos;
     b = hm / (Hq * U);
     h = (hm / U) % Hq;
     u = hm % U;
@@ -115,8 +96,9 @@ inline int prop_cut(long long total, const int* sizes, int n, int d) {
 // mapping; the paper's order is ascending); bit 10 = alternate the unit
 // direction per queue (queue d descending iff d is odd; single-queue
 // mappings are unaffected) -- see include/attn_numa.h ATTN_ORDER_ALTERNATE;
-// bit 11 = SHF with every ACC shared by all dies (kind-4 queues), bit 12 =
-// SHF with one die per ACC even where the library would share it (R23).
+// bit 11 = SHF with every ACC shared by all dies (one head-major queue: the
+// dies form one capacity domain), bit 12 = SHF with one die per ACC even
+// where the library would share it (R23).
 constexpr int kMapMask = 0xff;
 constexpr int kOrderDescending = 0x100;
 constexpr int kOrderAlternate = 0x400;
@@ -129,7 +111,9 @@ constexpr int kShfAccPerDie = 0x1000;
 // n_domains ACC K/V footprints live in that one L2.  When those footprints
 // exceed half of it (the capacity sweep: SHF's DRAM
 // bytes leave head-first's between 2 x 32 and 2 x 48 MiB per ACC on the
-// 126 MiB L2), swizzled head-first shares each ACC among the dies instead.
+// 126 MiB L2), swizzled head-first shares each ACC among the dies instead:
+// the whole GPU is one capacity domain, and SHF over one domain is the
+// head-major order.
 ATTN_HD bool shf_acc_shared(int n_domains, long long N, int d, long long l2_bytes) {
   const long long kv_acc = 2ll * N * d * 2;  // K and V of one KV head, bf16
   return n_domains > 1 && l2_bytes > 0 && (long long)n_domains * kv_acc > l2_bytes / 2;
@@ -154,7 +138,9 @@ inline bool build_queues(int mapping_arg, int B, int Hq, int Hkv, int U, int n_d
   const int G = Hq / Hkv;
   const int total = B * Hq * U;
   if (mapping < 0 || mapping > 3) return false;
-  if (mapping == 0 || mapping == 1 || n_domains == 1) {
+  // R23: SHF with shared ACCs = SHF over ONE capacity domain = head-first order
+  const bool one_domain = n_domains == 1 || (mapping == 2 && (mapping_arg & kShfAccShared));
+  if (mapping == 0 || mapping == 1 || one_domain) {
     const bool block_major = (mapping == 0 || mapping == 3);  // SBF on one die == BF
     sp.n_queues = 1;
     sp.steal = 0;
@@ -165,26 +151,6 @@ inline bool build_queues(int mapping_arg, int B, int Hq, int Hkv, int U, int n_d
   sp.n_queues = D;
   sp.steal = 1;
   for (int d = 0; d < D; ++d) sp.queue_of_domain[d] = d;
-  if (mapping == 2 && (mapping_arg & kShfAccShared)) {
-    // R23: every die takes its SM share of each period of S consecutive
-    // head-major units, spread over the period, so all dies serve the same
-    // ACC at the same time and at the same point of its causal prefix
-    sp.slot_T[D] = 0;
-    for (int d = D - 1; d >= 0; --d) {
-      if (sms_per_domain[d] < 0) return false;
-      sp.slot_T[d] = sp.slot_T[d + 1] + sms_per_domain[d];
-    }
-    const int S = sp.slot_T[0];
-    if (S <= 0) return false;
-    const int full = total / S, rem = total % S;
-    for (int d = 0; d < D; ++d) {
-      const int sd = sms_per_domain[d];
-      int tail = 0;  // owned slots in the partial last period
-      for (int r = 0; r < sd; ++r) tail += interleave_slot(sp.slot_T, d, r) < rem;
-      sp.q[d] = QueueDesc{4, 0, full * sd + tail, d, sd, S, 0};
-    }
-    return true;
-  }
   if (mapping == 3) {
     for (int d = 0; d < D; ++d) {
       const int ng = (Hkv > d) ? (Hkv - d + D - 1) / D : 0;  // groups g = d, d + D, ...

@@ -82,13 +82,13 @@ def test_swizzled_head_first_colocates_accs_on_device():
 
 
 def test_shared_acc_grain_on_device():
-    """R23: with the ACC shared, every ACC's units run on SMs of every die and
-    each unit is popped from the queue the mapping reference puts it in
-    (or stolen at the tail); the result is bit-identical to the per-die grain."""
+    """R23: with the ACC shared, the dies form one capacity domain: one queue
+    in head-major order (the mapping reference's), every ACC's units run on
+    SMs of both dies, and the result is bit-identical to the per-die grain."""
     t = attn_topology(0)
     if t["n_domains"] < 2:
         pytest.skip("probe found one domain")
-    B, Hq, Hkv, N, d = 1, 2, 2, 65536, 128  # 256 units per ACC: more than one period of 148
+    B, Hq, Hkv, N, d = 1, 2, 2, 65536, 128  # 256 units per ACC: more than one wave of 148 SMs
     tr, o_sh = _trace_run(B, Hq, Hkv, N, d, True, "swizzled_head_first:shared")
     _, o_pd = _trace_run(B, Hq, Hkv, N, d, True, "swizzled_head_first:per_die")
     assert torch.equal(o_sh.view(torch.int16), o_pd.view(torch.int16))
@@ -98,9 +98,9 @@ def test_shared_acc_grain_on_device():
     for qi, q in enumerate(queues):
         for (b, h, u) in q:
             rec = tr[(b * Hq + h) * U + u]
-            assert int(rec[5]) == qi or int(rec[6]) == 1
+            assert int(rec[5]) == qi == 0 and int(rec[6]) == 0
             doms[(b, h)].add(int(rec[4]))
-    assert all(len(s) == 2 for s in doms.values())
+    assert len(queues) == 1 and all(len(s) == 2 for s in doms.values())
 
 
 def test_shf_grain_rule_applied_by_the_library():
