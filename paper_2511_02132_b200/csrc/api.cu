@@ -68,8 +68,8 @@ struct DevState {
   unsigned long long slot_tick = 0;
   attn_trace_rec_t* trace = nullptr;
   long long trace_cap = 0;
-  bool attr_done[8] = {false, false, false, false, false, false, false, false};
-  int max_clusters[4] = {0, 0, 0, 0};  // co-resident CTA-pair clusters per forward variant
+  bool attr_done[16] = {};       // forward variants: [idx + 4 * cluster + 8 * ones-column row sum]
+  int max_clusters[8] = {};       // co-resident CTA-pair clusters per forward variant [idx + 4 * ones]
   bool pattr_done[2] = {false, false};  // attn_fwd_pair_kernel<causal>
   int pmax_clusters[2] = {0, 0};
   // e2e host-buffer path
@@ -461,10 +461,10 @@ int validate(const void* q, const void* k, const void* v, void* o, int B, int Hq
 
 // 3-D view [heads][N][d] of a [B][H][N][d] tensor: a box never crosses into
 // the next head, and rows >= N are out of bounds (zero-filled by TMA).
-int make_tmap(CUtensorMap* m, const void* base, long long heads, int N, int d, int box_rows) {
+int make_tmap(CUtensorMap* m, const void* base, long long heads, int N, int d, int box_rows, int box_cols = 64) {
   cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)N, (cuuint64_t)heads};
   cuuint64_t strides[2] = {(cuuint64_t)d * 2, (cuuint64_t)N * d * 2};
-  cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
+  cuuint32_t box[3] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -473,19 +473,20 @@ int make_tmap(CUtensorMap* m, const void* base, long long heads, int N, int d, i
   return ATTN_OK;
 }
 
-template <int D, bool kCausal>
+template <int D, bool kCausal, bool kOnesL = false>
 int launch_t(DevState& st, int attr_idx, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
              const KernelParams& kp, int grid, cudaStream_t s, bool cluster, int cluster_units) {
   const int smem = Cfg<D>::kSmemBytes;
+  const int ai = attr_idx + (kOnesL ? 8 : 0), ci = attr_idx + (kOnesL ? 4 : 0);
   if (!cluster) {
-    auto* fn = attn_fwd_sm100_kernel<D, kCausal, 1>;
-    if (!st.attr_done[attr_idx]) {
+    auto* fn = attn_fwd_sm100_kernel<D, kCausal, 1, kOnesL>;
+    if (!st.attr_done[ai]) {
       ATTN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      st.attr_done[attr_idx] = true;
+      st.attr_done[ai] = true;
     }
     fn<<<grid, kThreads, smem, s>>>(tq, tk, tv, kp);
   } else {
-    auto* fn = attn_fwd_sm100_kernel<D, kCausal, 2>;
+    auto* fn = attn_fwd_sm100_kernel<D, kCausal, 2, kOnesL>;
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -497,17 +498,17 @@ int launch_t(DevState& st, int attr_idx, const CUtensorMap& tq, const CUtensorMa
     cfg.stream = s;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (!st.attr_done[4 + attr_idx]) {
+    if (!st.attr_done[4 + ai]) {
       ATTN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       // persistent grid: as many pairs as can be co-resident (pairs need two
       // free SMs of one GPC, so this can be below num_sms / 2)
       cfg.gridDim = dim3(st.num_sms);
       int nc = 0;
       ATTN_CUDA(cudaOccupancyMaxActiveClusters(&nc, fn, &cfg));
-      st.max_clusters[attr_idx] = nc > 0 ? nc : st.num_sms / 2;
-      st.attr_done[4 + attr_idx] = true;
+      st.max_clusters[ci] = nc > 0 ? nc : st.num_sms / 2;
+      st.attr_done[4 + ai] = true;
     }
-    grid = 2 * std::min(st.max_clusters[attr_idx], cluster_units);
+    grid = 2 * std::min(st.max_clusters[ci], cluster_units);
     cfg.gridDim = dim3(grid);
     ATTN_CUDA(cudaLaunchKernelEx(&cfg, fn, tq, tk, tv, kp));
   }
@@ -516,6 +517,16 @@ int launch_t(DevState& st, int attr_idx, const CUtensorMap& tq, const CUtensorMa
   g_info.block = kThreads;
   g_info.smem_bytes = smem;
   return ATTN_OK;
+}
+
+// d < 64 forward: the row sum rides in the PV MMA (a ones column of V);
+// ATTN_ONES_L=0 in the environment keeps it on the softmax warps (comparison).
+bool use_ones_column() {
+  static const bool on = [] {
+    const char* e = getenv("ATTN_ONES_L");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 // d in (64, 128]: one query tile per SM, the unit's two tiles on a CTA pair
@@ -690,8 +701,15 @@ int fwd_impl(const void* q, const void* k, const void* v, void* o, int B, int Hq
   // (pair kernel): half the keys of K, half the head-dim columns of V
   const int k_box = (cluster || pair) ? kBlockN / 2 : kBlockN;
   const int v_box = cluster ? kBlockN / 2 : kBlockN;
-  if ((rc = make_tmap(&tk, k, (long long)B * Hkv, N, d, k_box)) != ATTN_OK) return rc;
-  if ((rc = make_tmap(&tv, v, (long long)B * Hkv, N, d, v_box)) != ATTN_OK) return rc;
+  // d < 64: K and V land d columns wide and the tensor core sums P into the
+  // spare column d of O (the row sum l; attn_fwd_sm100.cuh kOnesL).  That l
+  // sums the bf16-rounded P (as the numerator does), within 2^-9 relative of
+  // the fp32 sum; the backward's LSE input keeps the fp32 sum (attn_fwd_lse).
+  const bool ones = dpad == 64 && d < 64 && lse == nullptr && use_ones_column();
+  const int kv_cols = ones ? d : 64;
+  kp.kv_tx_bytes = kBlockN * kv_cols * 2 * (dpad / 64);
+  if ((rc = make_tmap(&tk, k, (long long)B * Hkv, N, d, k_box, kv_cols)) != ATTN_OK) return rc;
+  if ((rc = make_tmap(&tv, v, (long long)B * Hkv, N, d, v_box, kv_cols)) != ATTN_OK) return rc;
 
   const int total = B * Hq * U;
   const int cunits = B * Hsched * Usched;
@@ -701,6 +719,8 @@ int fwd_impl(const void* q, const void* k, const void* v, void* o, int B, int Hq
                 : launch_pair<false>(st, tq, tk, tv, kp, stream, total);
   else if (dpad == 128 && causal) rc = launch_t<128, true>(st, 0, tq, tk, tv, kp, grid, stream, cluster, cunits);
   else if (dpad == 128) rc = launch_t<128, false>(st, 1, tq, tk, tv, kp, grid, stream, cluster, cunits);
+  else if (causal && ones) rc = launch_t<64, true, true>(st, 2, tq, tk, tv, kp, grid, stream, cluster, cunits);
+  else if (ones) rc = launch_t<64, false, true>(st, 3, tq, tk, tv, kp, grid, stream, cluster, cunits);
   else if (causal) rc = launch_t<64, true>(st, 2, tq, tk, tv, kp, grid, stream, cluster, cunits);
   else rc = launch_t<64, false>(st, 3, tq, tk, tv, kp, grid, stream, cluster, cunits);
   if (rc != ATTN_OK) return rc;

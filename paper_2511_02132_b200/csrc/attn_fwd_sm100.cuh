@@ -142,6 +142,7 @@ struct KernelParams {
   __nv_bfloat16* o_dst[kMaxDst];
   int n_dst, Hq_out, h_off;
   float* lse;        // optional [B][Hq][N] natural-log row LSE (backward input), may be null
+  int kv_tx_bytes;   // bytes one K or V block lands in a CTA (kKVBytes, or 128 * d_real * 2 with kOnesL)
   SchedParams sched;
   int* counters;                 // one int per queue, 32 ints apart, then the done count
   const signed char* domain_of_smid;
@@ -315,7 +316,12 @@ __device__ __forceinline__ void run_scheduler(const KernelParams& p, CT* ctrl) {
 // to both, and each MMA warp releases a ring slot to both CTAs' kv_empty.  The
 // pair iterates over the longer unit's key blocks; the CTA whose own unit is
 // shorter (causal) only releases the extra slots.
-template <int D, bool kCausal, int kCl>
+// kOnesL (D = 64, d_real < 64): the row sum l is not accumulated by the
+// softmax but by the tensor core: K/V are loaded d_real columns wide, the
+// ring slots' column d_real holds 1.0 (columns beyond it 0, written once per
+// launch), so O += P V also accumulates O[:, d_real] = sum_k bf16(P_k) -- the
+// same P the numerator uses -- and the fix-up rescales it with O.
+template <int D, bool kCausal, int kCl, bool kOnesL>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                           const __grid_constant__ CUtensorMap tm_v, const KernelParams p) {
@@ -369,6 +375,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2) {
     ptx::tmem_alloc(&ctrl->tmem_base, kTmemCols);
     ptx::tmem_relinquish();
+  }
+  if constexpr (kOnesL) {
+    // K/V land d_real columns wide; logical column d_real of every ring slot
+    // row is 1.0 and the columns after it 0 (16-byte chunks d_real/8 .. 7 of
+    // each 128-byte row, at their 128B-swizzled positions).  Q keeps its
+    // zero-filled padding, so the 1.0 in K's column d_real adds nothing to S.
+    static_assert(!kOnesL || C::kChunks == 1, "ones column needs one swizzle atom per row");
+    const int c0 = p.d_real / 8;
+    for (int i = threadIdx.x; i < C::kStages * kBlockN * 8; i += kThreads) {
+      const int chunk = i & 7, rrow = i >> 3;  // rrow = slot * 128 + row
+      if (chunk < c0) continue;
+      uint4 val = make_uint4(0u, 0u, 0u, 0u);
+      if (chunk == c0) val.x = 0x3F80u;  // bf16 1.0 in the first element of the chunk
+      const int phys = chunk ^ (rrow & 7);
+      *reinterpret_cast<uint4*>(kv_smem + rrow * 128 + phys * 16) = val;
+    }
+    ptx::fence_proxy_async_smem();  // generic SMEM writes -> visible to TMA / tensor core
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -447,7 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_wait(&ctrl->kv_empty[kv_stage], kv_phase ^ 1);
             if constexpr (kCl > 1) {
               // this CTA's half of the block's rows, multicast into both CTAs
-              ptx::mbar_arrive_expect_tx(&ctrl->kv_full[kv_stage], C::kKVBytes);
+              ptx::mbar_arrive_expect_tx(&ctrl->kv_full[kv_stage], p.kv_tx_bytes);
               uint8_t* dst = kv_smem + kv_stage * C::kKVBytes + crank * (kBlockN / 2) * 128;
 #pragma unroll
               for (int c = 0; c < C::kChunks; ++c)
@@ -457,7 +480,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (++kv_stage == C::kStages) { kv_stage = 0; kv_phase ^= 1; }
               continue;
             }
-            ptx::mbar_arrive_expect_tx(&ctrl->kv_full[kv_stage], C::kKVBytes);
+            ptx::mbar_arrive_expect_tx(&ctrl->kv_full[kv_stage], p.kv_tx_bytes);
             uint8_t* dst = kv_smem + kv_stage * C::kKVBytes;
 #pragma unroll
             for (int c = 0; c < C::kChunks; ++c)
@@ -826,7 +849,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               pr.x = (k <= lim) ? pr.x : 0.f;
               pr.y = (k + 1 <= lim) ? pr.y : 0.f;
             }
-            sq[(k >> 1) & 3] = ptx::fadd2(sq[(k >> 1) & 3], pr);
+            if constexpr (!kOnesL) sq[(k >> 1) & 3] = ptx::fadd2(sq[(k >> 1) & 3], pr);
             r[k >> 1] = ptx::pack_bf16(pr.x, pr.y);
           }
           if constexpr (kSepP) {
@@ -851,17 +874,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         ATTN_CYC_ADD(2);
         if (diag) exp_block(std::true_type{});
         else exp_block(std::false_type{});
-        const float2 s01 = ptx::fadd2(sq[0], sq[1]), s23 = ptx::fadd2(sq[2], sq[3]);
-        const float2 s4 = ptx::fadd2(s01, s23);
-        const float sum = s4.x + s4.y;
-        l = (j == 0) ? sum : fmaf(l, alpha, sum);
+        if constexpr (!kOnesL) {
+          const float2 s01 = ptx::fadd2(sq[0], sq[1]), s23 = ptx::fadd2(sq[2], sq[3]);
+          const float2 s4 = ptx::fadd2(s01, s23);
+          const float sum = s4.x + s4.y;
+          l = (j == 0) ? sum : fmaf(l, alpha, sum);
+        }
         m = m_use;
         ATTN_CYC_ADD(3);
         ATTN_CYC_COUNT(7);
       }
       ATTN_CYC_START();
       // ---- epilogue: O / l -> bf16 -> global
-      if constexpr (kSplit == 2) {
+      if constexpr (kSplit == 2 && !kOnesL) {
         sred->lsum[t][quarter][hf][lane] = l;
         ptx::named_bar_sync(bar_id, 64);
         l += sred->lsum[t][quarter][hf ^ 1][lane];
@@ -869,6 +894,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ATTN_CYC_TIMED(6, ptx::mbar_wait(&ctrl->o_ready[t], o_phase));
       o_phase ^= 1;
       ptx::tc_fence_after();
+      if constexpr (kOnesL) l = __uint_as_float(ptx::tmem_ld1(trow + C::col_o(t) + p.d_real));
       const float inv_l = 1.f / l;
       if (p.lse != nullptr && hf == 0 && qb * kBlockM + row < p.N)  // lse = scale*m + ln(l)
         p.lse[(long long)(e.x * p.Hq + hh) * p.N + qb * kBlockM + row] = (m * c + __log2f(l)) * 0.6931471805599453f;
