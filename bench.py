@@ -410,6 +410,15 @@ def run_ours(a):
     sustained = peak_sus is not None and timed_s >= 1.0
     peak = peak_sus if sustained else peak_burst
     achieved = flops_rank / (ms_kernel * 1e-3) / 1e12
+    # exp-unit ceiling: one exp2 per (row, key) for 4d
+    # forward flops (10d backward); MUFU.EX2 16 per clock per SM (measured,
+    # scripts/micro/mufu_rate.cu) with 1 in 8 exps on the FMA-pipe polynomial
+    # (x 8/7), at the maximum SM clock.  Below the tensor peak (d <= 64) the
+    # kernel is ALU-bound and the roofline uses it.
+    exp_per_clk_sm = 16.0 * 8.0 / 7.0
+    flops_per_exp = (10.0 if a.pass_ == "bwd" else 4.0) * d
+    max_mhz = clocks.get("sm_max_mhz") or 1965
+    exp_ceiling = exp_per_clk_sm * topo["num_sms"] * max_mhz * 1e6 * flops_per_exp / 1e12
     main_ncu = by_mapping.get(variant_key(*main_var), {})
     traffic = None
     if main_ncu.get("dram_gb_per_launch") is not None:
@@ -428,9 +437,16 @@ def run_ours(a):
                    "parallelism": f"heads sharded over {world} GPU(s), no data-path collective",
                    "l2": l2_note, "flop_convention": ("4*B*Hq*N^2*d, causal x0.5" if a.pass_ == "fwd" else
                                                       "10*B*Hq*N^2*d (5 matmuls), causal x0.5")},
-        "roofline": {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
-                     "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "peak_source": (f"bf16_tflops_sustained {peak_src} (timed region {timed_s:.1f} s of "
+        "roofline": {"bound": "tensor" if exp_ceiling >= peak else "alu", "achieved": round(achieved, 1),
+                     "peak": round(min(peak, exp_ceiling), 1), "unit": "TFLOP/s",
+                     "frac": round(achieved / min(peak, exp_ceiling), 4), "traffic": traffic,
+                     "tensor_peak": peak,
+                     "exp_ceiling": round(exp_ceiling, 1),
+                     "exp_ceiling_source": f"16 MUFU.EX2/clk/SM x 8/7 (1/8 polynomial) x {topo['num_sms']} SMs x "
+                                           f"{max_mhz} MHz x {flops_per_exp:.0f} flop per exp",
+                     "peak_source": ("exp_ceiling (the exps bound this head dim, DESIGN.md section 6)"
+                                     if exp_ceiling < peak else
+                                     f"bf16_tflops_sustained {peak_src} (timed region {timed_s:.1f} s of "
                                      f"back-to-back launches)" if sustained else
                                      f"bf16_tflops {peak_src} (burst: timed region {timed_s:.2f} s)"),
                      "frac_of_burst": round(achieved / peak_burst, 4),
