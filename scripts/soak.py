@@ -27,7 +27,8 @@ for s in shapes:
     q, k, v = synth.make_qkv(B, Hq, Hkv, N, d, base=hash(s) & 0xFFFF, device="cuda")
     ref = attn_fwd(q, k, v, causal=causal, mapping="block_first")
     data[s] = (q, k, v, ref)
-maps = ["block_first", "head_first", "swizzled_head_first", "swizzled_block_first"]
+maps = ["block_first", "head_first", "swizzled_head_first", "swizzled_block_first", "swizzled_head_first:shared",
+        "swizzled_head_first:per_die"]
 n = bad = 0
 t0 = time.time()
 outs = []
