@@ -25,15 +25,14 @@
 // that writes the output.  The same threshold-rescale rule, P and O += P V
 // as the two-tiles-per-CTA kernel; only l's summation order differs.
 //
-// One tile per SM alone would need 160 KB of SMEM traffic per 1024 tensor
-// cycles (Q and K read by S, V by O += P V, K and V written by TMA: more than
-// the 128 B/clk an SM's shared memory delivers).  The unit's two tiles (query
-// blocks 2u, 2u+1) therefore run on the two SMs of a cluster as ONE M = 256
-// tile: the leader CTA's MMA warp issues tcgen05.mma.cta_group::2, each SM
+// The unit's two tiles (query blocks 2u, 2u+1) run on the two SMs of a
+// cluster as ONE M = 256 tile: the leader CTA's MMA warp issues
+// tcgen05.mma.cta_group::2, each SM
 // supplies its own 128 rows of Q (A) and HALF of the B operand -- keys
 // 64r..64r+63 of K_j for S, head-dim columns 64r..64r+63 of V_j for O += P V
-// -- so each SM reads and stores half of every K/V block (96 KB per 1024
-// cycles).  Both SMs' TMA loads signal the leader's barriers (cta_group::2
+// -- so each SM loads and the tensor core reads half of every K/V block
+// (ncu, C2: tensor-pipe SMEM wavefronts 26% of peak vs 50% in the two-tile
+// kernel).  Both SMs' TMA loads signal the leader's barriers (cta_group::2
 // TMA); both SMs' softmax warps publish P to the leader; the leader's commits
 // multicast to both.  The leader's scheduler warp pops units from the
 // mapping's queues (the plain per-unit queues: B * Hq * U entries).
