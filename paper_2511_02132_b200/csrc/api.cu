@@ -700,9 +700,7 @@ int fwd_impl(const void* q, const void* k, const void* v, void* o, int B, int Hq
   // clusters: each CTA loads half the rows of every K/V block; CTA-pair MMA
   // (pair kernel): half the keys of K, half the head-dim columns of V
   const int k_box = (cluster || pair) ? kBlockN / 2 : kBlockN;
-  // (CTA-pair MMA at D = 128, ATTN_PAIR_MMA: each CTA loads the head-dim half
-  // of V over all 128 keys)
-  const int v_box = (cluster && !(ATTN_PAIR_MMA && dpad == 128)) ? kBlockN / 2 : kBlockN;
+  const int v_box = cluster ? kBlockN / 2 : kBlockN;
   // d < 64: K and V land d columns wide and the tensor core sums P into the
   // spare column d of O (the row sum l; attn_fwd_sm100.cuh kOnesL).  That l
   // sums the bf16-rounded P (as the numerator does), within 2^-9 relative of

@@ -79,9 +79,6 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units; see DESIGN.md "fix-up"
 #ifndef ATTN_SETMAXNREG
 #define ATTN_SETMAXNREG 1
 #endif
-#ifndef ATTN_PAIR_MMA
-#define ATTN_PAIR_MMA 0  // 1: CTA-pair clusters at D = 128 use cta_group::2 MMAs (measured slower)
-#endif
 
 constexpr int kEmuPeriod = ATTN_EMU_PERIOD;  // every kEmuPeriod-th exp2 pair runs on the FMA pipe (0: none)
 // Head dim <= 64: half the tensor work per exp, so the exps bound the kernel
@@ -247,24 +244,6 @@ __device__ __forceinline__ int pair_kv_blocks(const int4& e, const KernelParams&
              unit_kv_blocks<kCausal>(2 * e.z + 1 < p.U ? 2 * e.z + 1 : -1, p.nblk));
 }
 
-// kCl == 2 at D = 128 (k2sm): the pair's two SMs compute tile t of both
-// CTAs' units as ONE M = 256 tensor-core tile (tcgen05.mma.cta_group::2), so
-// tile t runs for the longer of the two CTAs' tile t; the CTA whose tile is
-// shorter (or missing) publishes all-zero P rows for the extra blocks.
-template <bool kCausal>
-__device__ __forceinline__ int cta_tile_blocks(const int4& e, int r, int t, const KernelParams& p) {
-  int h;
-  const int u = own_unit<2>(e, (uint32_t)r, p.U, p.pair_heads, h);
-  if (u < 0) return 0;
-  int n0, n1;
-  unit_blocks<kCausal>(u, p.nblk, n0, n1);
-  return t == 0 ? n0 : n1;
-}
-template <bool kCausal>
-__device__ __forceinline__ int pair_tile_blocks(const int4& e, int t, const KernelParams& p) {
-  return max(cta_tile_blocks<kCausal>(e, 0, t, p), cta_tile_blocks<kCausal>(e, 1, t, p));
-}
-
 // The scheduler warp (lane 0): pop this SM's die queue (or the shared one),
 // steal from the others when it runs dry, and broadcast (b, h, unit) to the
 // CTA's consumers through the 2-entry SMEM ring; kCl == 2: the leader CTA
@@ -356,19 +335,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   Ctrl* ctrl = reinterpret_cast<Ctrl*>(smem + C::kOffCtrl);
   [[maybe_unused]] SplitRed* sred = reinterpret_cast<SplitRed*>(smem + C::kOffCtrl + 1024);
   static_assert(sizeof(Ctrl) <= 1024, "control block exceeds 1 KB");
-  static_assert(C::kStages <= 16 && (!(kCl == 2 && D == 128) || 2 * C::kStages <= 16),
-                "K/V ring deeper than the Ctrl barrier arrays");
+  static_assert(C::kStages <= 16, "K/V ring deeper than the Ctrl barrier arrays");
   static_assert(kSplit == 1 || C::kCtrlBytes >= 1024 + (int)sizeof(SplitRed), "split reductions do not fit");
   static_assert(C::kSmemBytes <= 232448, "shared memory exceeds 227 KB");
 
   static_assert(kCl == 1 || kCl == 2, "cluster size 1 or 2");
   constexpr bool kSepP = ATTN_SEP_P && D <= 64 && kCl == 1;
-  // CTA pairs at D = 128: cta_group::2 MMAs (M = 256) over both SMs; each SM
-  // holds its own Q tiles and HALF of every K/V block (keys 64r.. of K,
-  // head-dim columns 64r.. of V) in half-size ring slots (twice as many)
-  constexpr bool k2sm = ATTN_PAIR_MMA && kCl == 2 && D == 128;
-  constexpr int kSlotBytes = k2sm ? C::kKVBytes / 2 : C::kKVBytes;
-  constexpr int kNStages = k2sm ? 2 * C::kStages : C::kStages;
   static_assert(!kSepP || 256 + 2 * D + 128 <= kTmemCols, "separate P does not fit in TMEM");
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -379,20 +351,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < kSchedRing; ++i) {
       ptx::mbar_init(&ctrl->sched_full[i], 1);
       // TMA + MMA + softmax warps (one arrive each), of every CTA of the cluster
-      // (k2sm: the peer's MMA warp reads no entries)
-      ptx::mbar_init(&ctrl->sched_empty[i], kCl * (2 + kSoftmaxWarps) - (k2sm ? 1 : 0));
+      ptx::mbar_init(&ctrl->sched_empty[i], kCl * (2 + kSoftmaxWarps));
     }
     ptx::mbar_init(&ctrl->q_full, 1);
     ptx::mbar_init(&ctrl->q_empty, 1);
-    for (int i = 0; i < kNStages; ++i) {
+    for (int i = 0; i < C::kStages; ++i) {
       ptx::mbar_init(&ctrl->kv_full[i], 1);
-      // released by the MMA warp of every CTA of the cluster (k2sm: the leader's, multicast)
-      ptx::mbar_init(&ctrl->kv_empty[i], k2sm ? 1 : kCl);
+      ptx::mbar_init(&ctrl->kv_empty[i], kCl);  // released by the MMA warp of every CTA of the cluster
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&ctrl->s_ready[i], 1);
       for (int h = 0; h < kPParts; ++h)
-        ptx::mbar_init(&ctrl->p_ready[i][h], 4 * kSplit * (k2sm ? 2 : 1));  // softmax warps of the tile (both SMs: k2sm)
+        ptx::mbar_init(&ctrl->p_ready[i][h], 4 * kSplit);  // one arrive per softmax warp of the tile
       ptx::mbar_init(&ctrl->o_ready[i], 1);
       ptx::mbar_init(&ctrl->s_free[i], 4 * kSplit);
       ptx::mbar_init(&ctrl->p_free[i], 1);
@@ -405,13 +375,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tma_prefetch_desc(&tm_v);
   }
   if (warp == 2) {
-    if constexpr (k2sm) {  // one warp of each CTA of the pair
-      ptx::tmem_alloc_2(&ctrl->tmem_base, kTmemCols);
-      ptx::tmem_relinquish_2();
-    } else {
-      ptx::tmem_alloc(&ctrl->tmem_base, kTmemCols);
-      ptx::tmem_relinquish();
-    }
+    ptx::tmem_alloc(&ctrl->tmem_base, kTmemCols);
+    ptx::tmem_relinquish();
   }
   if constexpr (kOnesL) {
     // K/V land d_real columns wide; logical column d_real of every ring slot
@@ -475,42 +440,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           ++seq;
         }
-        if constexpr (k2sm) {
-          const int np = max(pair_tile_blocks<kCausal>(e, 0, p), pair_tile_blocks<kCausal>(e, 1, p));
-          // Q: both tiles of both CTAs, every unit, on the leader's q_full (a
-          // missing unit / tile reads rows >= N: zero-filled, never stored)
-          ptx::mbar_wait(&ctrl->q_empty, q_phase ^ 1);
-          q_phase ^= 1;
-          if (crank == 0) ptx::mbar_arrive_expect_tx(&ctrl->q_full, 2 * 2 * C::kQTileBytes);
-          const uint32_t lead_q = ptx::mapa_shared(ptx::smem_u32(&ctrl->q_full), 0);
-          for (int t = 0; t < 2; ++t) {
-            const int bh = b * p.Hq + h, row = (u >= 0 ? 2 * u + t : 2 * p.U + t) * kBlockM;
-#pragma unroll
-            for (int c = 0; c < C::kChunks; ++c)
-              ptx::tma_load_3d_2sm(q_smem + t * C::kQTileBytes + c * kBlockM * 128, &tm_q, lead_q, c * 64, row, bh,
-                                   pol_q);
-          }
-          const int kvbh = b * p.Hkv + h / p.G;
-          for (int j = 0; j < np; ++j) {
-#pragma unroll
-            for (int which = 0; which < 2; ++which) {
-              ptx::mbar_wait(&ctrl->kv_empty[kv_stage], kv_phase ^ 1);
-              if (crank == 0) ptx::mbar_arrive_expect_tx(&ctrl->kv_full[kv_stage], 2 * kSlotBytes);
-              const uint32_t full = ptx::mapa_shared(ptx::smem_u32(&ctrl->kv_full[kv_stage]), 0);
-              uint8_t* dst = kv_smem + kv_stage * kSlotBytes;
-              if (which == 0) {  // keys 64r..64r+63 of K_j, both 64-column atoms
-#pragma unroll
-                for (int c = 0; c < C::kChunks; ++c)
-                  ptx::tma_load_3d_2sm(dst + c * (kBlockN / 2) * 128, &tm_k, full, c * 64,
-                                       j * kBlockN + (int)crank * (kBlockN / 2), kvbh, pol_kv);
-              } else {  // head-dim columns 64r..64r+63 of V_j, all 128 keys
-                ptx::tma_load_3d_2sm(dst, &tm_v, full, (int)crank * 64, j * kBlockN, kvbh, pol_kv);
-              }
-              if (++kv_stage == kNStages) { kv_stage = 0; kv_phase ^= 1; }
-            }
-          }
-          continue;
-        }
         if (n_own > 0) {
         ptx::mbar_wait(&ctrl->q_empty, q_phase ^ 1);
         q_phase ^= 1;
@@ -566,9 +495,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       if constexpr (kCl > 1) {
         // drain: every slot's last fill released by both CTAs, so no remote
         // commit is still in flight towards this CTA when it exits
-        for (int i = 0; i < kNStages; ++i) {
+        for (int i = 0; i < C::kStages; ++i) {
           ptx::mbar_wait(&ctrl->kv_empty[kv_stage], kv_phase ^ 1);
-          if (++kv_stage == kNStages) { kv_stage = 0; kv_phase ^= 1; }
+          if (++kv_stage == C::kStages) { kv_stage = 0; kv_phase ^= 1; }
         }
       }
     }
@@ -579,108 +508,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (ATTN_SETMAXNREG) ptx::setmaxnreg_dec<kOtherRegs>();
     const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(&ctrl->tmem_base);
     SchedReader<kCl> sr;
-    if constexpr (k2sm) {
-      // The leader issues every MMA of the pair (M = 256: rows 0-127 in this
-      // SM, 128-255 in the peer); B operands are split: keys 0-63 of K_j in
-      // the leader's half slot and 64-127 in the peer's (S), head-dim columns
-      // 0-63 / 64-127 of V_j likewise (O += P V).  The peer's warp 1 idles.
-      if (crank == 0) {
-        constexpr uint32_t idesc_s2 = ptx::idesc_bf16_f32(2 * kBlockM, kBlockN, 0, 0);
-        constexpr uint32_t idesc_o2 = ptx::idesc_bf16_f32(2 * kBlockM, D, 0, 1);
-        const uint64_t dq0 = ptx::smem_desc_sw128(ptx::smem_u32(q_smem), 16, 1024);
-        const uint64_t dk0 = ptx::smem_desc_sw128(ptx::smem_u32(kv_smem), 16, 1024);
-        const uint64_t dv0 = ptx::smem_desc_sw128(ptx::smem_u32(kv_smem), kBlockN * 128, 1024);
-        uint32_t q_phase = 0, p_phase0 = 0, p_phase1 = 0;
-        int kv_stage = 0;
-        uint32_t kv_phase = 0;
-        auto issue_s2 = [&](int t, int slot) {
-          const uint64_t dq = dq0 + (uint64_t)((t * C::kQTileBytes) >> 4);
-          const uint64_t dk = dk0 + (uint64_t)((slot * kSlotBytes) >> 4);
-#pragma unroll
-          for (int k = 0; k < D / 16; ++k) {
-            const uint32_t oq = ((k >> 2) * (kBlockM * 128) + (k & 3) * 32) >> 4;
-            const uint32_t ok = ((k >> 2) * (kBlockN / 2 * 128) + (k & 3) * 32) >> 4;
-            ptx::mma_ss_2(tmem + C::col_s(t), dq + oq, dk + ok, idesc_s2, k > 0 ? 1u : 0u);
-          }
-        };
-        auto issue_pv2 = [&](int t, int slot, bool acc, int h) {
-          const uint64_t dv = dv0 + (uint64_t)((slot * kSlotBytes) >> 4);
-#pragma unroll
-          for (int k = h * (8 / kPParts); k < (h + 1) * (8 / kPParts); ++k)
-            ptx::mma_ts_2(tmem + C::col_o(t), tmem + C::col_s(t) + k * 8, dv + (uint64_t)((k * 16 * 128) >> 4),
-                          idesc_o2, (acc || k > 0) ? 1u : 0u);
-        };
-        auto take2 = [&]() {
-          const int st = kv_stage;
-          ptx::mbar_wait(&ctrl->kv_full[st], kv_phase);
-          if (++kv_stage == kNStages) { kv_stage = 0; kv_phase ^= 1; }
-          return st;
-        };
-        while (true) {
-          const int4 e = sr.next(ctrl, false);
-          __syncwarp();
-          if (lane == 0) sr.release_prev(ctrl);
-          if (!e.w) break;
-          const int n0 = pair_tile_blocks<kCausal>(e, 0, p), n1 = pair_tile_blocks<kCausal>(e, 1, p);
-          const int n = n0 > n1 ? n0 : n1;
-          ptx::mbar_wait(&ctrl->q_full, q_phase);
-          q_phase ^= 1;
-          int sK = take2();
-          ptx::tc_fence_after();
-          if (ptx::elect_one_sync()) {
-            if (n0 > 0) {
-              issue_s2(0, sK);
-              ptx::mma_commit_2mc(&ctrl->s_ready[0], kMask);
-            }
-            if (n1 > 0) {
-              issue_s2(1, sK);
-              ptx::mma_commit_2mc(&ctrl->s_ready[1], kMask);
-            }
-            ptx::mma_commit_2mc(&ctrl->kv_empty[sK], kMask);
-            if (n == 1) ptx::mma_commit_2mc(&ctrl->q_empty, kMask);
-          }
-          __syncwarp();
-          for (int j = 0; j < n; ++j) {
-            const int sV = take2();
-            const bool nxt = j + 1 < n;
-            if (nxt) sK = take2();
-            ptx::tc_fence_after();
-#pragma unroll
-            for (int t = 0; t < 2; ++t) {
-              const int nt = (t == 0) ? n0 : n1;
-              if (j < nt) {
-                const uint32_t ph = (t == 0) ? p_phase0 : p_phase1;
-#pragma unroll
-                for (int h = 0; h < kPParts; ++h) {
-                  ptx::mbar_wait_cluster(&ctrl->p_ready[t][h], ph);  // both SMs' softmax warps
-                  ptx::tc_fence_after();
-                  if (ptx::elect_one_sync()) issue_pv2(t, sV, j > 0, h);
-                  __syncwarp();
-                }
-                if (t == 0) p_phase0 ^= 1; else p_phase1 ^= 1;
-                if (ptx::elect_one_sync()) {
-                  if (j + 1 < nt) {
-                    issue_s2(t, sK);
-                    ptx::mma_commit_2mc(&ctrl->s_ready[t], kMask);
-                  } else {
-                    ptx::mma_commit_2mc(&ctrl->o_ready[t], kMask);
-                  }
-                }
-                __syncwarp();
-              }
-            }
-            if (ptx::elect_one_sync()) {
-              ptx::mma_commit_2mc(&ctrl->kv_empty[sV], kMask);
-              if (nxt) {
-                ptx::mma_commit_2mc(&ctrl->kv_empty[sK], kMask);
-                if (j + 2 == n) ptx::mma_commit_2mc(&ctrl->q_empty, kMask);
-              }
-            }
-            __syncwarp();
-          }
-        }
-      }
-    } else {
     constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(kBlockM, kBlockN, 0, 0);
     constexpr uint32_t idesc_o = ptx::idesc_bf16_f32(kBlockM, D, 0, 1);
     // descriptors at k = 0; advancing K by 16 elements adds 32 B (2 in the
@@ -881,7 +708,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         extra_blocks = 0;
       }
     }
-    }  // !k2sm
   } else if (warp == 2) {
     // --------------------------------------------------------------- scheduler
     if (ATTN_SETMAXNREG) ptx::setmaxnreg_dec<kOtherRegs>();
@@ -921,16 +747,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       int n0 = 0, n1 = 0;
       if (u >= 0) unit_blocks<kCausal>(u, p.nblk, n0, n1);
       const int nt = (t == 0) ? n0 : n1;
-      // k2sm: the pair's M = 256 tile t runs for the longer CTA's tile; this
-      // tile's blocks j >= nt are all-masked (P = 0: O, m and l unchanged)
-      const int ntp = k2sm ? pair_tile_blocks<kCausal>(e, t, p) : nt;
-      if (ntp == 0) continue;
+      if (nt == 0) continue;
       const int qb = 2 * u + t;
       // keys of the last key block that exist (ragged N): local key k < tail_keys
       const int last_blk = p.nblk - 1;
       const int tail_lim = (p.N - last_blk * kBlockN - 1) - cbase;  // last block: local k visible iff k <= tail_lim
       float m = -INFINITY, l = 0.f;
-      for (int j = 0; j < ntp; ++j, ++gblk) {
+      for (int j = 0; j < nt; ++j, ++gblk) {
         ATTN_CYC_START();
         ptx::mbar_wait(&ctrl->s_ready[t], s_phase);
         ATTN_CYC_ADD(0);
@@ -949,7 +772,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         int lim = kCols;
         if (kCausal && j == qb) lim = row - cbase;
         if (j == last_blk && tail_lim < lim) lim = tail_lim;
-        if (k2sm && j >= nt) lim = -1;
         // warp-uniform choice between the masked and the unmasked loop bodies
         const bool diag = __any_sync(0xffffffffu, lim < kCols - 1);
         if (diag) {  // masked keys -> -inf
@@ -1048,11 +870,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::tmem_wait_st();
           ptx::tc_fence_before();
           __syncwarp();
-          if constexpr (k2sm) {
-            if (lane == 0) ptx::mbar_arrive_cluster_relaxed(ptx::mapa_shared(ptx::smem_u32(&ctrl->p_ready[t][h]), 0));
-          } else {
-            if (lane == 0) ptx::mbar_arrive(&ctrl->p_ready[t][h]);
-          }
+          if (lane == 0) ptx::mbar_arrive(&ctrl->p_ready[t][h]);
         }
         };
         ATTN_CYC_ADD(2);
@@ -1080,13 +898,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::tc_fence_after();
       if constexpr (kOnesL) l = __uint_as_float(ptx::tmem_ld1(trow + C::col_o(t) + p.d_real));
       const float inv_l = 1.f / l;
-      if (p.lse != nullptr && hf == 0 && nt > 0 && qb * kBlockM + row < p.N)  // lse = scale*m + ln(l)
+      if (p.lse != nullptr && hf == 0 && qb * kBlockM + row < p.N)  // lse = scale*m + ln(l)
         p.lse[(long long)(e.x * p.Hq + hh) * p.N + qb * kBlockM + row] = (m * c + __log2f(l)) * 0.6931471805599453f;
       const long long orow =
           ((long long)(e.x * p.Hq_out + p.h_off + hh) * p.N + (long long)qb * kBlockM + row) * p.d_real + hf * kOCols;
       // real columns of this thread's slice (multiple of 8); rows >= N (ragged
       // last query block) store nothing but still join the warp-wide TMEM loads
-      const int ncol = (nt > 0 && qb * kBlockM + row < p.N) ? p.d_real - hf * kOCols : 0;
+      const int ncol = (qb * kBlockM + row < p.N) ? p.d_real - hf * kOCols : 0;
 #pragma unroll
       for (int cc = 0; cc < kOCols; cc += 32) {
         uint32_t o[32];
@@ -1121,8 +939,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if constexpr (kCl > 1) ptx::cluster_sync();  // no remote SMEM access may target an exited CTA
   if (warp == 2) {
     ptx::tc_fence_after();
-    if constexpr (k2sm) ptx::tmem_dealloc_2(*reinterpret_cast<volatile uint32_t*>(&ctrl->tmem_base), kTmemCols);
-    else ptx::tmem_dealloc(*reinterpret_cast<volatile uint32_t*>(&ctrl->tmem_base), kTmemCols);
+    ptx::tmem_dealloc(*reinterpret_cast<volatile uint32_t*>(&ctrl->tmem_base), kTmemCols);
   }
 }
 
