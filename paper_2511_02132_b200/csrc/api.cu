@@ -80,7 +80,7 @@ struct DevState {
   size_t bbuf_bytes[9] = {};
   bool e2e_ready = false;
   bool battr_done[8] = {false, false, false, false, false, false, false, false};
-  cudaStream_t e2e_stream[3] = {nullptr, nullptr, nullptr};
+  cudaStream_t e2e_stream[4] = {nullptr, nullptr, nullptr, nullptr};  // H2D, compute (even chunks), D2H, compute (odd)
   cudaEvent_t e2e_ev[2][kE2EChunks + 1] = {};
 };
 
@@ -957,7 +957,7 @@ int attn_fwd_host(const void* q_host, const void* k_host, const void* v_host, vo
       }
     }
     if (!st.e2e_ready) {
-      for (int i = 0; i < 3; ++i) ATTN_CUDA(cudaStreamCreateWithFlags(&st.e2e_stream[i], cudaStreamNonBlocking));
+      for (int i = 0; i < 4; ++i) ATTN_CUDA(cudaStreamCreateWithFlags(&st.e2e_stream[i], cudaStreamNonBlocking));
       for (int i = 0; i < kE2EChunks + 1; ++i)
         for (int j = 0; j < 2; ++j) ATTN_CUDA(cudaEventCreateWithFlags(&st.e2e_ev[j][i], cudaEventDisableTiming));
       st.e2e_ready = true;
@@ -972,11 +972,14 @@ int attn_fwd_host(const void* q_host, const void* k_host, const void* v_host, vo
   target = std::min(target, tg);
   int gpc = (tg + target - 1) / target;  // KV groups per chunk
   gpc = std::min(gpc, Hkv);
-  cudaStream_t cin = st.e2e_stream[0], comp = st.e2e_stream[1], cout = st.e2e_stream[2];
+  // consecutive chunks compute on two streams, so chunk i+1's persistent CTAs
+  // take the SMs chunk i's tail leaves idle (heads are independent)
+  cudaStream_t cin = st.e2e_stream[0], cout = st.e2e_stream[2];
+  const cudaStream_t comps[2] = {st.e2e_stream[1], st.e2e_stream[3]};
   cudaEvent_t* ev_in = st.e2e_ev[0];
   cudaEvent_t* ev_k = st.e2e_ev[1];
   ATTN_CUDA(cudaEventRecord(ev_in[kE2EChunks], s));  // order after the caller's prior work
-  for (cudaStream_t x : {cin, comp, cout}) ATTN_CUDA(cudaStreamWaitEvent(x, ev_in[kE2EChunks], 0));
+  for (cudaStream_t x : {cin, comps[0], comps[1], cout}) ATTN_CUDA(cudaStreamWaitEvent(x, ev_in[kE2EChunks], 0));
   char* dq = static_cast<char*>(st.hbuf[0]);
   char* dk = static_cast<char*>(st.hbuf[1]);
   char* dv = static_cast<char*>(st.hbuf[2]);
@@ -988,6 +991,7 @@ int attn_fwd_host(const void* q_host, const void* k_host, const void* v_host, vo
       const size_t qoff = ((size_t)b * Hq + (size_t)g0 * G) * row_bytes, qlen = (size_t)gn * G * row_bytes;
       const size_t koff = ((size_t)b * Hkv + g0) * row_bytes, klen = (size_t)gn * row_bytes;
       const int e = c % kE2EChunks;
+      const cudaStream_t comp = comps[c & 1];
       if (c >= kE2EChunks) ATTN_CUDA(cudaStreamWaitEvent(cin, ev_k[e], 0));  // slot's previous chunk consumed
       ATTN_CUDA(cudaMemcpyAsync(dq + qoff, static_cast<const char*>(q_host) + qoff, qlen, cudaMemcpyHostToDevice, cin));
       ATTN_CUDA(cudaMemcpyAsync(dk + koff, static_cast<const char*>(k_host) + koff, klen, cudaMemcpyHostToDevice, cin));
@@ -1037,7 +1041,7 @@ int attn_bwd_host(const void* q_host, const void* k_host, const void* v_host, co
       }
     }
     if (!st.e2e_ready) {
-      for (int i = 0; i < 3; ++i) ATTN_CUDA(cudaStreamCreateWithFlags(&st.e2e_stream[i], cudaStreamNonBlocking));
+      for (int i = 0; i < 4; ++i) ATTN_CUDA(cudaStreamCreateWithFlags(&st.e2e_stream[i], cudaStreamNonBlocking));
       for (int i = 0; i < kE2EChunks + 1; ++i)
         for (int j = 0; j < 2; ++j) ATTN_CUDA(cudaEventCreateWithFlags(&st.e2e_ev[j][i], cudaEventDisableTiming));
       st.e2e_ready = true;
@@ -1052,11 +1056,14 @@ int attn_bwd_host(const void* q_host, const void* k_host, const void* v_host, co
   target = std::min(target, tg);
   int gpc = (tg + target - 1) / target;  // KV groups per chunk
   gpc = std::min(gpc, Hkv);
-  cudaStream_t cin = st.e2e_stream[0], comp = st.e2e_stream[1], cout = st.e2e_stream[2];
+  // consecutive chunks compute on two streams, so chunk i+1's persistent CTAs
+  // take the SMs chunk i's tail leaves idle (heads are independent)
+  cudaStream_t cin = st.e2e_stream[0], cout = st.e2e_stream[2];
+  const cudaStream_t comps[2] = {st.e2e_stream[1], st.e2e_stream[3]};
   cudaEvent_t* ev_in = st.e2e_ev[0];
   cudaEvent_t* ev_k = st.e2e_ev[1];
   ATTN_CUDA(cudaEventRecord(ev_in[kE2EChunks], s));  // order after the caller's prior work
-  for (cudaStream_t x : {cin, comp, cout}) ATTN_CUDA(cudaStreamWaitEvent(x, ev_in[kE2EChunks], 0));
+  for (cudaStream_t x : {cin, comps[0], comps[1], cout}) ATTN_CUDA(cudaStreamWaitEvent(x, ev_in[kE2EChunks], 0));
   char* b[9];
   for (int i = 0; i < 9; ++i) b[i] = static_cast<char*>(st.bbuf[i]);
   const char* hin[6] = {static_cast<const char*>(q_host), static_cast<const char*>(k_host),
@@ -1072,6 +1079,7 @@ int attn_bwd_host(const void* q_host, const void* k_host, const void* v_host, co
       const size_t loff = ((size_t)bi * Hq + (size_t)g0 * G) * lrow_bytes, llen = (size_t)gn * G * lrow_bytes;
       const size_t off[6] = {qoff, koff, koff, qoff, qoff, loff}, len[6] = {qlen, klen, klen, qlen, qlen, llen};
       const int e = c % kE2EChunks;
+      const cudaStream_t comp = comps[c & 1];
       if (c >= kE2EChunks) ATTN_CUDA(cudaStreamWaitEvent(cin, ev_k[e], 0));  // the event slot's previous chunk ran
       for (int i = 0; i < 6; ++i)
         ATTN_CUDA(cudaMemcpyAsync(b[i] + off[i], hin[i] + off[i], len[i], cudaMemcpyHostToDevice, cin));
@@ -1249,7 +1257,7 @@ void attn_shutdown(void) {
       st.bbuf_bytes[i] = 0;
     }
     if (st.e2e_ready) {
-      for (int i = 0; i < 3; ++i) cudaStreamDestroy(st.e2e_stream[i]);
+      for (int i = 0; i < 4; ++i) cudaStreamDestroy(st.e2e_stream[i]);
       for (int j = 0; j < 2; ++j)
         for (int i = 0; i < kE2EChunks + 1; ++i) cudaEventDestroy(st.e2e_ev[j][i]);
       st.e2e_ready = false;
