@@ -221,32 +221,38 @@ int measure_reread(attn_topology_t& t, const std::vector<int>& present, const st
     for (int l = 0; l < L; ++l) mean[dm][l] /= cnt[dm];
   size_t l2 = (size_t)t.l2_bytes;
   void* flush = nullptr;
-  int *d_claimed = nullptr;
+  int* d_claimed = nullptr;
   uint32_t* d_rr = nullptr;
-  ATTN_CUDA(cudaMalloc(&flush, 2 * l2));
-  ATTN_CUDA(cudaMalloc(&d_claimed, sizeof(int)));
-  ATTN_CUDA(cudaMalloc(&d_rr, sizeof(uint32_t) * L));
   std::vector<double> near_rr, far_rr;
-  for (int dm = 0; dm < 2; ++dm) {
-    int target = -1;
-    for (int s : present)
-      if (t.domain_of_smid[s] == dm) { target = s; break; }
-    ATTN_CUDA(cudaMemset(flush, dm + 1, 2 * l2));  // evict the probe lines from L2
-    ATTN_CUDA(cudaMemset(d_claimed, 0, sizeof(int)));
-    ATTN_CUDA(cudaMemset(d_rr, 0xFF, sizeof(uint32_t) * L));
-    topo_reread_kernel<<<8 * t.num_sms, 32>>>(d_probe, d_claimed, target, d_rr);
-    ATTN_CUDA(cudaGetLastError());
-    ATTN_CUDA(cudaDeviceSynchronize());
-    std::vector<uint32_t> rr(L);
-    ATTN_CUDA(cudaMemcpy(rr.data(), d_rr, sizeof(uint32_t) * L, cudaMemcpyDeviceToHost));
-    for (int l = 0; l < L; ++l) {
-      if (rr[l] == 0xFFFFFFFFu) continue;  // target SM never ran a CTA (cannot happen with 8 CTAs per SM)
-      (mean[dm][l] > mean[1 - dm][l] ? far_rr : near_rr).push_back(rr[l]);
+  // the scratch buffers are freed on every path out of the measurement
+  auto measure = [&]() -> int {
+    ATTN_CUDA(cudaMalloc(&flush, 2 * l2));
+    ATTN_CUDA(cudaMalloc(&d_claimed, sizeof(int)));
+    ATTN_CUDA(cudaMalloc(&d_rr, sizeof(uint32_t) * L));
+    for (int dm = 0; dm < 2; ++dm) {
+      int target = -1;
+      for (int s : present)
+        if (t.domain_of_smid[s] == dm) { target = s; break; }
+      ATTN_CUDA(cudaMemset(flush, dm + 1, 2 * l2));  // evict the probe lines from L2
+      ATTN_CUDA(cudaMemset(d_claimed, 0, sizeof(int)));
+      ATTN_CUDA(cudaMemset(d_rr, 0xFF, sizeof(uint32_t) * L));
+      topo_reread_kernel<<<8 * t.num_sms, 32>>>(d_probe, d_claimed, target, d_rr);
+      ATTN_CUDA(cudaGetLastError());
+      ATTN_CUDA(cudaDeviceSynchronize());
+      std::vector<uint32_t> rr(L);
+      ATTN_CUDA(cudaMemcpy(rr.data(), d_rr, sizeof(uint32_t) * L, cudaMemcpyDeviceToHost));
+      for (int l = 0; l < L; ++l) {
+        if (rr[l] == 0xFFFFFFFFu) continue;  // target SM never ran a CTA (cannot happen with 8 CTAs per SM)
+        (mean[dm][l] > mean[1 - dm][l] ? far_rr : near_rr).push_back(rr[l]);
+      }
     }
-  }
-  cudaFree(flush);
-  cudaFree(d_claimed);
-  cudaFree(d_rr);
+    return ATTN_OK;
+  };
+  const int mrc = measure();
+  if (flush) cudaFree(flush);
+  if (d_claimed) cudaFree(d_claimed);
+  if (d_rr) cudaFree(d_rr);
+  if (mrc != ATTN_OK) return mrc;
   if (near_rr.empty() || far_rr.empty()) return ATTN_OK;
   std::sort(near_rr.begin(), near_rr.end());
   std::sort(far_rr.begin(), far_rr.end());
@@ -530,8 +536,9 @@ bool use_ones_column() {
 }
 
 // d in (64, 128]: one query tile per SM, the unit's two tiles on a CTA pair
-// (attn_fwd_pair.cuh) when ATTN_FWD_PAIR=1 in the environment (work in
-// progress); otherwise the two-tiles-per-CTA kernel.
+// (attn_fwd_pair.cuh) when ATTN_FWD_PAIR=1 in the environment (an
+// experiment, slower than the default: DESIGN.md section 6); otherwise the
+// two-tiles-per-CTA kernel.
 bool use_pair_kernel() {
   static const bool on = [] {
     const char* e = getenv("ATTN_FWD_PAIR");
