@@ -59,6 +59,7 @@ NCU_METRICS = ("gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_wr
                "lts__t_sector_hit_rate.pct", "lts__t_sector_op_read_hit_rate.pct", "lts__t_sectors.sum",
                "lts__t_sectors_srcunit_ltcfabric.sum",
                "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+               "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
                "sm__cycles_elapsed.avg.per_second")
 
 
@@ -231,6 +232,7 @@ def ncu_measure(shape, variants, device: int, timeout_s: float):
             "l2_hit_rate_pct": vals.get("lts__t_sector_hit_rate.pct"),
             "l2_read_hit_rate_pct": vals.get("lts__t_sector_op_read_hit_rate.pct"),
             "tensor_pipe_pct": vals.get("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"),
+            "xu_pipe_pct": vals.get("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"),  # MUFU (exp2)
             "hbm_gbs": round(dram / t / 1e9, 1) if dram and t else None,
             "dram_gb_per_launch": round(dram / 1e9, 3) if dram is not None else None,
             "cross_die_gb_per_launch": round(fab * 32 / 1e9, 3) if fab is not None else None,
