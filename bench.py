@@ -344,7 +344,8 @@ def run_ours(a):
     # interleaved rounds (one step of every variant per round, median over
     # rounds) so every variant sees the same thermal / power-cap state; the
     # value variant's own line above is the contract's timed region
-    rounds = max(3, a.steps // 4)
+    # about 2 s of steps per variant (at least 5 rounds, at most 200)
+    rounds = max(5, min(200, int(2000.0 / max(ms_step, 1e-3))))
     per_var = {v: [] for v in variants}
     for v in variants:  # one untimed step each (descriptors, first-touch)
         step(0, v)
