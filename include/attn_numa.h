@@ -126,6 +126,15 @@ typedef enum {
 #define ATTN_SHF_ACC_SHARED 0x800
 #define ATTN_SHF_ACC_PER_DIE 0x1000
 
+/* OR into `mapping` (attn_bwd / attn_bwd_host; the forward ignores it): run
+ * the two-pass backward whose dq is bit-reproducible.  Without it, head dims
+ * d <= 64 use the single-pass kernel (csrc/attn_bwd_fused_sm100.cuh), which
+ * computes P and dS once and accumulates dq with fp32 reduce-adds in L2 in
+ * arrival order: dq may then differ in the last bits between runs and
+ * between mappings (dk and dv stay bit-identical).  d > 64 always runs the
+ * two-pass backward. */
+#define ATTN_BWD_DETERMINISTIC 0x2000
+
 typedef enum {
   ATTN_OK = 0,
   ATTN_ERR_INVALID_VALUE = 1, /* null pointer, size <= 0, Hq % Hkv != 0, bad mapping value,
@@ -195,8 +204,11 @@ ATTN_API int attn_fwd_lse(const void* q, const void* k, const void* v, void* o, 
  * [B][Hq][N] from attn_fwd_lse; dq [B][Hq][N][d], dk, dv [B][Hkv][N][d]: device
  * bf16 outputs, fully written (GQA: dk, dv sum over the group's query heads).
  * `mapping` orders the work units exactly as for the forward (dQ: query
- * blocks of a head; dK/dV: key blocks of a KV group).  Three launches:
- * rowsum(dO o O) into library workspace, the dQ kernel, the dK/dV kernel.
+ * blocks of a head; dK/dV: key blocks of a KV group).  Launches:
+ * rowsum(dO o O) into per-call library workspace, then either the dQ kernel
+ * and the dK/dV kernel (d > 64, or ATTN_BWD_DETERMINISTIC), or, for d <= 64,
+ * a zero fill of a per-call fp32 dq accumulator [B][Hq][N][64] (4*B*Hq*N*64
+ * bytes of workspace), the single-pass kernel and a dq conversion kernel.
  * Same validation and status codes as attn_fwd (ATTN_ORDER_DESCENDING
  * applies; ATTN_CLUSTER_MULTICAST returns ATTN_ERR_UNSUPPORTED: the
  * backward has no cluster variant); gradients must not overlap each other or

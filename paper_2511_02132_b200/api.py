@@ -41,6 +41,7 @@ SHF_ACC_SHARED = 0x800  # include/attn_numa.h ATTN_SHF_ACC_SHARED
 SHF_ACC_PER_DIE = 0x1000  # include/attn_numa.h ATTN_SHF_ACC_PER_DIE
 # "swizzled_head_first:shared" / ":per_die" force the SHF ACC grain (R23); no suffix = library rule
 SHF_ACC = {"": 0, "shared": SHF_ACC_SHARED, "per_die": SHF_ACC_PER_DIE}
+BWD_DETERMINISTIC = 0x2000  # include/attn_numa.h ATTN_BWD_DETERMINISTIC (two-pass backward, reproducible dq)
 
 
 def _mapping_id(mapping, order: str = "ascending", cluster: bool = False) -> int:
@@ -187,9 +188,12 @@ def attn_fwd_lse(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: b
 def attn_bwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor, dout: torch.Tensor,
              lse: torch.Tensor, *, causal: bool = False, scale: Optional[float] = None,
              mapping="swizzled_head_first", order: str = "ascending", stream: Optional[torch.cuda.Stream] = None,
-             dq: Optional[torch.Tensor] = None, dk: Optional[torch.Tensor] = None, dv: Optional[torch.Tensor] = None):
+             dq: Optional[torch.Tensor] = None, dk: Optional[torch.Tensor] = None, dv: Optional[torch.Tensor] = None,
+             deterministic: bool = False):
     """Gradients (dq, dk, dv) of sum(dout * attention(q, k, v)) (PAPER.md eq:ba), bf16.
-    dq / dk / dv may be passed as preallocated outputs (shaped like q / k / v)."""
+    dq / dk / dv may be passed as preallocated outputs (shaped like q / k / v).
+    deterministic=True selects the two-pass backward (bit-reproducible dq) for
+    d <= 64, where the default single-pass kernel adds dq in arrival order."""
     B, Hq, Hkv, N, d = _qkv_shape(q, k, v)
     _check_tensor("o", o, q.shape)
     _check_tensor("dout", dout, q.shape)
@@ -204,16 +208,18 @@ def attn_bwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor,
     lib = _lib.load()
     _check(lib.attn_bwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), dout.data_ptr(), lse.data_ptr(),
                         dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), B, Hq, Hkv, N, d, int(bool(causal)),
-                        float(scale), _mapping_id(mapping, order), _stream_ptr(stream)))
+                        float(scale), _mapping_id(mapping, order) | (BWD_DETERMINISTIC if deterministic else 0),
+                        _stream_ptr(stream)))
     return dq, dk, dv
 
 
 def attn_bwd_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor, dout: torch.Tensor,
                   lse: torch.Tensor, dq: torch.Tensor, dk: torch.Tensor, dv: torch.Tensor, *, causal: bool = False,
                   scale: Optional[float] = None, mapping="swizzled_head_first", order: str = "ascending",
-                  stream: Optional[torch.cuda.Stream] = None):
+                  stream: Optional[torch.cuda.Stream] = None, deterministic: bool = False):
     """End-to-end backward on HOST (ideally pinned) tensors: H2D of q, k, v, o,
-    dout (bf16) and lse (fp32), the backward kernels, D2H of dq, dk, dv, sync."""
+    dout (bf16) and lse (fp32), the backward kernels, D2H of dq, dk, dv, sync.
+    deterministic as attn_bwd."""
     B, Hq, Hkv, N, d = _qkv_shape(q, k, v, cuda=False)
     for name, t, shape in (("o", o, q.shape), ("dout", dout, q.shape), ("dq", dq, q.shape), ("dk", dk, k.shape),
                            ("dv", dv, k.shape)):
@@ -224,7 +230,9 @@ def attn_bwd_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Te
     lib = _lib.load()
     _check(lib.attn_bwd_host(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), dout.data_ptr(),
                              lse.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), B, Hq, Hkv, N, d,
-                             int(bool(causal)), float(scale), _mapping_id(mapping, order), _stream_ptr(stream)))
+                             int(bool(causal)), float(scale),
+                             _mapping_id(mapping, order) | (BWD_DETERMINISTIC if deterministic else 0),
+                             _stream_ptr(stream)))
     return dq, dk, dv
 
 

@@ -16,6 +16,7 @@
 
 #include "../../include/attn_numa.h"
 #include "attn_bwd_sm100.cuh"
+#include "attn_bwd_fused_sm100.cuh"
 #include "attn_fwd_sm100.cuh"
 #include "attn_fwd_pair.cuh"
 #include "attn_sched.h"
@@ -80,6 +81,10 @@ struct DevState {
   size_t bbuf_bytes[9] = {};
   bool e2e_ready = false;
   bool battr_done[8] = {false, false, false, false, false, false, false, false};
+  bool fattr_done[2] = {false, false};  // attn_bwd_fused_kernel<64, causal>
+  // stream-ordered pool for per-call backward workspace (rowsum(dO o O), the
+  // fp32 dQ accumulator); keeps freed blocks mapped (release threshold max)
+  cudaMemPool_t ws_pool = nullptr;
   cudaStream_t e2e_stream[4] = {nullptr, nullptr, nullptr, nullptr};  // H2D, compute (even chunks), D2H, compute (odd)
   cudaEvent_t e2e_ev[2][kE2EChunks + 1] = {};
 };
@@ -446,10 +451,10 @@ int validate(const void* q, const void* k, const void* v, void* o, int B, int Hq
   if (B <= 0 || Hq <= 0 || Hkv <= 0 || N <= 0 || d <= 0) return fail(ATTN_ERR_INVALID_VALUE, "size <= 0");
   if (Hq % Hkv != 0) return fail(ATTN_ERR_INVALID_VALUE, "Hq % Hkv != 0 (non-uniform GQA groups)");
   if ((mapping & ~(kMapMask | kOrderDescending | kOrderAlternate | ATTN_CLUSTER_MULTICAST | kShfAccShared |
-                   kShfAccPerDie)) || (mapping & kMapMask) > 3)
+                   kShfAccPerDie | ATTN_BWD_DETERMINISTIC)) || (mapping & kMapMask) > 3)
     return fail(ATTN_ERR_INVALID_VALUE,
                 "mapping not in {0,1,2,3} (| ATTN_ORDER_DESCENDING | ATTN_ORDER_ALTERNATE | ATTN_CLUSTER_MULTICAST | "
-                "ATTN_SHF_ACC_SHARED | ATTN_SHF_ACC_PER_DIE)");
+                "ATTN_SHF_ACC_SHARED | ATTN_SHF_ACC_PER_DIE | ATTN_BWD_DETERMINISTIC)");
   if ((mapping & kShfAccShared) && (mapping & kShfAccPerDie))
     return fail(ATTN_ERR_INVALID_VALUE, "ATTN_SHF_ACC_SHARED and ATTN_SHF_ACC_PER_DIE are exclusive");
   if (!std::isfinite(scale)) return fail(ATTN_ERR_INVALID_VALUE, "non-finite scale");
@@ -467,6 +472,20 @@ int validate(const void* q, const void* k, const void* v, void* o, int B, int Hq
 
 // 3-D view [heads][N][d] of a [B][H][N][d] tensor: a box never crosses into
 // the next head, and rows >= N are out of bounds (zero-filled by TMA).
+// fp32 [heads][N][d] view with boxes of box_rows x 32 floats (one 128-B
+// swizzle row): the dQ accumulator of the fused backward (TMA reduce-add).
+int make_tmap_f32(CUtensorMap* m, void* base, long long heads, int N, int d, int box_rows) {
+  cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)N, (cuuint64_t)heads};
+  cuuint64_t strides[2] = {(cuuint64_t)d * 4, (cuuint64_t)N * d * 4};
+  cuuint32_t box[3] = {32, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(ATTN_ERR_CUDA, "cuTensorMapEncodeTiled (fp32) failed (" + std::to_string((int)r) + ")");
+  return ATTN_OK;
+}
+
 int make_tmap(CUtensorMap* m, const void* base, long long heads, int N, int d, int box_rows, int box_cols = 64) {
   cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)N, (cuuint64_t)heads};
   cuuint64_t strides[2] = {(cuuint64_t)d * 2, (cuuint64_t)N * d * 2};
@@ -760,6 +779,36 @@ int launch_bwd_t(DevState& st, const CUtensorMap& tq, const CUtensorMap& tdo, co
   return ATTN_OK;
 }
 
+template <bool kCausal>
+int launch_bwd_fused(DevState& st, const CUtensorMap& tq, const CUtensorMap& tdo, const CUtensorMap& tk,
+                     const CUtensorMap& tv, const CUtensorMap& tacc, const bwd::BwdParams& pkv, int grid,
+                     cudaStream_t s) {
+  auto* fn = bwd::attn_bwd_fused_kernel<64, kCausal>;
+  constexpr int smem = bwd::FCfg<64>::kSmemBytes;
+  if (!st.fattr_done[kCausal ? 1 : 0]) {
+    ATTN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    st.fattr_done[kCausal ? 1 : 0] = true;
+  }
+  fn<<<grid, bwd::kThreadsF, smem, s>>>(tq, tdo, tk, tv, tacc, pkv);
+  ATTN_CUDA(cudaGetLastError());
+  return ATTN_OK;
+}
+
+// The library's stream-ordered workspace pool on `dev` (created on first use).
+int ws_pool(DevState& st, int dev, cudaMemPool_t* out) {
+  if (!st.ws_pool) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    ATTN_CUDA(cudaMemPoolCreate(&st.ws_pool, &props));
+    cuuint64_t thr = ~0ull;
+    ATTN_CUDA(cudaMemPoolSetAttribute(st.ws_pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  }
+  *out = st.ws_pool;
+  return ATTN_OK;
+}
+
 int bwd_impl(const void* q, const void* k, const void* v, const void* o, const void* dout, const float* lse, void* dq,
              void* dk, void* dv, int B, int Hq, int Hkv, int N, int d, int causal, float scale, int mapping,
              cudaStream_t stream) {
@@ -793,8 +842,29 @@ int bwd_impl(const void* q, const void* k, const void* v, const void* o, const v
   // the order of `stream` (stream-ordered pool), so concurrent backward calls
   // on other streams never share it.
   const size_t rows = (size_t)B * Hq * N;
+  const int dpad = d <= 64 ? 64 : 128;
+  const bool fused = dpad == 64 && !(mapping & ATTN_BWD_DETERMINISTIC);
+  mapping &= ~ATTN_BWD_DETERMINISTIC;
+  cudaMemPool_t pool = nullptr;
+  if ((rc = ws_pool(st, dev, &pool)) != ATTN_OK) return rc;
   float* dvec = nullptr;
-  ATTN_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dvec), rows * sizeof(float), stream));
+  float* dq_acc = nullptr;  // fused path: fp32 [B*Hq][N][64]
+  // two-pass: rowsum(dO o O) per row; fused: -lse2 / -D in blocks of 128 rows (attn_bwd_prep_kernel)
+  const int nblk_ws = (N + bwd::kBM - 1) / bwd::kBM;
+  const size_t vec_floats = fused ? (size_t)B * Hq * nblk_ws * 2 * bwd::kBM : rows;
+  ATTN_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&dvec), vec_floats * sizeof(float), pool, stream));
+  if (fused) {
+    if (cudaError_t e = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&dq_acc), rows * dpad * sizeof(float), pool,
+                                                stream);
+        e != cudaSuccess) {
+      cudaFreeAsync(dvec, stream);
+      return cuda_fail(e, "dq accumulator allocation");
+    }
+  }
+  auto free_ws = [&]() {
+    cudaFreeAsync(dvec, stream);
+    if (dq_acc) cudaFreeAsync(dq_acc, stream);
+  };
   const int nblk = (N + bwd::kBM - 1) / bwd::kBM;
   bwd::BwdParams pq{};
   pq.B = B; pq.Hq = Hq; pq.Hkv = Hkv; pq.N = N; pq.G = Hq / Hkv; pq.nblk = nblk; pq.d_real = d;
@@ -812,36 +882,61 @@ int bwd_impl(const void* q, const void* k, const void* v, const void* o, const v
   pkv.U = nblk;
   if (!build_sched(mapping, B, Hq, Hkv, nblk, st.active.n_domains, st.active.sms_per_domain, pq.sched) ||
       !build_sched(mapping, B, Hkv, Hkv, nblk, st.active.n_domains, st.active.sms_per_domain, pkv.sched)) {
-    cudaFreeAsync(dvec, stream);
+    free_ws();
     return fail(ATTN_ERR_INVALID_VALUE, "cannot build the schedule");
   }
   // the dQ and dK/dV grids run one after the other on `stream`: one slot
   pq.counters = pkv.counters = st.d_counters + (size_t)counter_slot(st, stream) * kCounterInts;
-  CUtensorMap tq, tdo, tk, tv;
+  CUtensorMap tq, tdo, tk, tv, tacc;
   if ((rc = make_tmap(&tq, q, (long long)B * Hq, N, d, bwd::kBM)) != ATTN_OK ||
       (rc = make_tmap(&tdo, dout, (long long)B * Hq, N, d, bwd::kBM)) != ATTN_OK ||
       (rc = make_tmap(&tk, k, (long long)B * Hkv, N, d, bwd::kBM)) != ATTN_OK ||
-      (rc = make_tmap(&tv, v, (long long)B * Hkv, N, d, bwd::kBM)) != ATTN_OK) {
-    cudaFreeAsync(dvec, stream);
+      (rc = make_tmap(&tv, v, (long long)B * Hkv, N, d, bwd::kBM)) != ATTN_OK ||
+      (fused && (rc = make_tmap_f32(&tacc, dq_acc, (long long)B * Hq, N, dpad, bwd::kBM)) != ATTN_OK)) {
+    free_ws();
     return rc;
   }
   const long long nrows = (long long)rows;
-  bwd::attn_bwd_dot_kernel<<<(unsigned)((nrows + 7) / 8), 256, 0, stream>>>(
-      reinterpret_cast<const __nv_bfloat16*>(o), reinterpret_cast<const __nv_bfloat16*>(dout), dvec, nrows, d);
+  if (fused) {
+    const long long prows = (long long)B * Hq * nblk * bwd::kBM;
+    bwd::attn_bwd_prep_kernel<<<(unsigned)((prows + 7) / 8), 256, 0, stream>>>(
+        reinterpret_cast<const __nv_bfloat16*>(o), reinterpret_cast<const __nv_bfloat16*>(dout), lse, dvec,
+        (long long)B * Hq, N, nblk, d);
+  } else {
+    bwd::attn_bwd_dot_kernel<<<(unsigned)((nrows + 7) / 8), 256, 0, stream>>>(
+        reinterpret_cast<const __nv_bfloat16*>(o), reinterpret_cast<const __nv_bfloat16*>(dout), dvec, nrows, d);
+  }
   if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) {
-    cudaFreeAsync(dvec, stream);
-    return cuda_fail(e, "attn_bwd_dot_kernel launch");
+    free_ws();
+    return cuda_fail(e, "attn_bwd_dot_kernel / attn_bwd_prep_kernel launch");
   }
   const int grid_q = std::min(st.num_sms, B * Hq * nblk), grid_kv = std::min(st.num_sms, B * Hkv * nblk);
-  const int dpad = d <= 64 ? 64 : 128;
-  if (dpad == 128 && causal) rc = launch_bwd_t<128, true>(st, tq, tdo, tk, tv, pq, pkv, grid_q, grid_kv, stream);
-  else if (dpad == 128) rc = launch_bwd_t<128, false>(st, tq, tdo, tk, tv, pq, pkv, grid_q, grid_kv, stream);
-  else if (causal) rc = launch_bwd_t<64, true>(st, tq, tdo, tk, tv, pq, pkv, grid_q, grid_kv, stream);
-  else rc = launch_bwd_t<64, false>(st, tq, tdo, tk, tv, pq, pkv, grid_q, grid_kv, stream);
-  cudaFreeAsync(dvec, stream);  // after the dQ and dK/dV kernels in stream order
+  if (fused) {
+    if (cudaError_t e = cudaMemsetAsync(dq_acc, 0, rows * dpad * sizeof(float), stream); e != cudaSuccess) {
+      free_ws();
+      return cuda_fail(e, "dq accumulator zero fill");
+    }
+    rc = causal ? launch_bwd_fused<true>(st, tq, tdo, tk, tv, tacc, pkv, grid_kv, stream)
+                : launch_bwd_fused<false>(st, tq, tdo, tk, tv, tacc, pkv, grid_kv, stream);
+    if (rc == ATTN_OK) {
+      const long long work = (long long)rows * (d / 8);
+      bwd::attn_bwd_dq_convert_kernel<<<(unsigned)((work + 255) / 256), 256, 0, stream>>>(
+          dq_acc, reinterpret_cast<__nv_bfloat16*>(dq), (long long)rows, d, dpad, scale);
+      if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) rc = cuda_fail(e, "attn_bwd_dq_convert_kernel launch");
+    }
+  } else if (dpad == 128 && causal) {
+    rc = launch_bwd_t<128, true>(st, tq, tdo, tk, tv, pq, pkv, grid_q, grid_kv, stream);
+  } else if (dpad == 128) {
+    rc = launch_bwd_t<128, false>(st, tq, tdo, tk, tv, pq, pkv, grid_q, grid_kv, stream);
+  } else if (causal) {
+    rc = launch_bwd_t<64, true>(st, tq, tdo, tk, tv, pq, pkv, grid_q, grid_kv, stream);
+  } else {
+    rc = launch_bwd_t<64, false>(st, tq, tdo, tk, tv, pq, pkv, grid_q, grid_kv, stream);
+  }
+  free_ws();  // after the kernels in stream order
   if (rc != ATTN_OK) return rc;
-  g_info.kernel_launches = 3;
-  g_info.units = B * Hq * nblk + B * Hkv * nblk;
+  g_info.kernel_launches = 3;  // D, then fused + dq convert (after a memset) or dQ + dK/dV
+  g_info.units = fused ? B * Hkv * nblk : B * Hq * nblk + B * Hkv * nblk;
   return ATTN_OK;
 }
 
@@ -1252,6 +1347,12 @@ void attn_shutdown(void) {
     if (st.d_domain) cudaFree(st.d_domain);
     if (st.d_counters) cudaFree(st.d_counters);
     for (bool& a : st.battr_done) a = false;
+    for (bool& a : st.fattr_done) a = false;
+    if (st.ws_pool) {
+      cudaDeviceSynchronize();  // per-call workspace is freed in stream order
+      cudaMemPoolDestroy(st.ws_pool);
+      st.ws_pool = nullptr;
+    }
     for (int i = 0; i < 4; ++i)
       if (st.hbuf[i]) cudaFree(st.hbuf[i]);
     cudaSetDevice(prev);

@@ -92,6 +92,8 @@ struct __align__(16) BCtrl {
   uint64_t dp_ready, ds_ready;          // dP in TMEM, dS stored (bf16, TMEM)
   uint64_t q_ready;                     // dQ: Q and dO copied into TMEM
   uint64_t s_free, dv_done;             // dKdV: S^T read into registers; dV MMA done (P^T SMEM free)
+  uint64_t dk_done;                     // fused: dK and dQ MMAs done (dS^T SMEM free)
+  uint64_t dq_full[2], dq_empty[2];     // fused: dQ TMEM buffers (MMA -> drain -> MMA)
   int4 entry[kSchedRing];
   uint32_t tmem_base;
 };

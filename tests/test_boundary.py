@@ -34,6 +34,17 @@ def test_header_exports_match(lib):
     assert declared <= exported
 
 
+def test_header_flag_values_match_binding():
+    """Every mapping flag the binding ORs in has the value the header defines."""
+    from paper_2511_02132_b200 import api
+
+    hdr = open(os.path.join(ROOT, "include", "attn_numa.h")).read()
+    defs = {m.group(1): int(m.group(2), 16) for m in re.finditer(r"#define ATTN_(\w+) (0x[0-9a-fA-F]+)", hdr)}
+    for name in ("ORDER_DESCENDING", "CLUSTER_MULTICAST", "ORDER_ALTERNATE", "SHF_ACC_SHARED", "SHF_ACC_PER_DIE",
+                 "BWD_DETERMINISTIC"):
+        assert defs[name] == getattr(api, name), name
+
+
 def test_status_strings_and_version(lib):
     assert lib.attn_status_string(0) == b"ATTN_OK"
     assert lib.attn_status_string(1) == b"ATTN_ERR_INVALID_VALUE"
@@ -48,7 +59,7 @@ def _fwd(lib, q=1 << 20, k=2 << 20, v=3 << 20, o=4 << 20, B=1, Hq=2, Hkv=2, N=12
 
 @pytest.mark.parametrize("kw,status", [
     (dict(q=0), 1), (dict(o=0), 1), (dict(B=0), 1), (dict(N=-1), 1), (dict(Hq=6, Hkv=4), 1),
-    (dict(mapping=4), 1), (dict(mapping=-1), 1), (dict(mapping=0x2000), 1), (dict(mapping=0x804), 1), (dict(mapping=0x404), 1), (dict(mapping=0x204), 1), (dict(mapping=0x104), 1), (dict(scale=float("nan")), 1), (dict(scale=float("inf")), 1),
+    (dict(mapping=4), 1), (dict(mapping=-1), 1), (dict(mapping=0x4000), 1), (dict(mapping=0x804), 1), (dict(mapping=0x404), 1), (dict(mapping=0x204), 1), (dict(mapping=0x104), 1), (dict(scale=float("nan")), 1), (dict(scale=float("inf")), 1),
     (dict(d=100), 2), (dict(d=136), 2), (dict(scale=-0.5), 2), (dict(q=(1 << 20) + 8), 2),
     (dict(o=(1 << 20) + 64), 1),   # o overlaps q
 ])

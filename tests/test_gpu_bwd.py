@@ -5,7 +5,10 @@ bf16 P / dS operands with fp32 accumulation, so errors scale with the
 gradient's own magnitude: max |g - g_ref| <= 2e-2 * max(1, max|g_ref|) and
 mean |g - g_ref| <= 2e-3 * max(1, mean|g_ref|) + 2^-9 * mean|g_ref| per tensor
 (the last term is the gradient's own bf16 rounding, reading R21).  The row LSE from
-attn_fwd_lse: |lse - lse_ref| <= 1e-3.  Every mapping gives the same bits.
+attn_fwd_lse: |lse - lse_ref| <= 1e-3.  The two-pass backward (d > 64, or
+deterministic=True) gives the same bits under every mapping; the single-pass
+one (d <= 64, attn_bwd_fused_sm100.cuh) does for dk and dv, while its dq sums
+fp32 tiles in arrival order and is checked against the oracle.
 """
 import math
 
@@ -34,13 +37,19 @@ CASES = [
 ]
 
 
-@pytest.mark.parametrize("B,Hq,Hkv,N,d,causal", CASES)
-def test_backward_matches_oracle(B, Hq, Hkv, N, d, causal):
+@pytest.mark.parametrize("deterministic", [False, True])
+@pytest.mark.parametrize("B,Hq,Hkv,N,d,causal", CASES + [
+    (1, 3, 1, 77, 8, True),        # one ragged block, tiny head dim (single-pass path)
+    (1, 4, 2, 1000, 32, False),    # non-causal wrap-around block order, GQA
+])
+def test_backward_matches_oracle(B, Hq, Hkv, N, d, causal, deterministic):
+    if d > 64 and not deterministic:
+        pytest.skip("d > 64 always runs the two-pass backward")
     q, k, v = synth.make_qkv(B, Hq, Hkv, N, d, base=31, device="cuda")
     do = synth.make_tensor("q", B, Hq, N, d, base=32, device="cuda")
     scale = 1.0 / math.sqrt(d)
     o, lse = attn_fwd_lse(q, k, v, causal=causal, scale=scale)
-    dq, dk, dv = attn_bwd(q, k, v, o, do, lse, causal=causal, scale=scale)
+    dq, dk, dv = attn_bwd(q, k, v, o, do, lse, causal=causal, scale=scale, deterministic=deterministic)
     torch.cuda.synchronize()
     rq, rk, rv, rl = oa.attention_bwd(q.cpu(), k.cpu(), v.cpu(), do.cpu(), causal=causal, scale=scale)
     assert np.abs(lse.cpu().numpy() - rl).max() <= 1e-3
@@ -61,6 +70,33 @@ def test_backward_bitexact_across_mappings():
             assert torch.equal(a.view(torch.int16), b.view(torch.int16)), m
 
 
+def test_backward_d64_mappings():
+    """d <= 64: deterministic=True is bit-identical across mappings; the
+    single-pass default keeps dk, dv bit-identical across mappings (each key
+    block's query blocks are summed in TMEM in a fixed order), and for causal
+    attention equal to the two-pass result bit for bit (same operands, same
+    block order); its dq agrees with the two-pass dq to bf16 rounding."""
+    q, k, v = synth.make_qkv(2, 8, 2, 640, 64, base=35, device="cuda")
+    do = synth.make_tensor("q", 2, 8, 640, 64, base=36, device="cuda")
+    o, lse = attn_fwd_lse(q, k, v, causal=True)
+    det = attn_bwd(q, k, v, o, do, lse, causal=True, mapping="block_first", deterministic=True)
+    fused = attn_bwd(q, k, v, o, do, lse, causal=True, mapping="block_first")
+    torch.cuda.synchronize()
+    for a, b in zip(fused[1:], det[1:]):
+        assert torch.equal(a.view(torch.int16), b.view(torch.int16))
+    dqd = (fused[0].float() - det[0].float()).abs()
+    assert dqd.max().item() <= 2.0 ** -7 * max(1.0, det[0].float().abs().max().item())
+    assert dqd.mean().item() <= 2.0 ** -9 * det[0].float().abs().mean().item()
+    for m in ("head_first", "swizzled_head_first", "swizzled_block_first"):
+        got_det = attn_bwd(q, k, v, o, do, lse, causal=True, mapping=m, deterministic=True)
+        got = attn_bwd(q, k, v, o, do, lse, causal=True, mapping=m)
+        torch.cuda.synchronize()
+        for a, b in zip(got_det, det):
+            assert torch.equal(a.view(torch.int16), b.view(torch.int16)), m
+        for a, b in zip(got[1:], fused[1:]):
+            assert torch.equal(a.view(torch.int16), b.view(torch.int16)), m
+
+
 @pytest.mark.parametrize("B,Hq,Hkv,N,d,causal", [
     (1, 4, 2, 300, 128, True),      # one chunk
     (2, 16, 8, 8192, 128, True),    # several pipelined chunks (>= 48 MB moved)
@@ -74,12 +110,31 @@ def test_bwd_host_path_bitexact(B, Hq, Hkv, N, d, causal):
     q, k, v = synth.make_qkv(B, Hq, Hkv, N, d, base=31, device="cuda")
     do = synth.make_tensor("q", B, Hq, N, d, base=32, device="cuda")
     o, lse = attn_fwd_lse(q, k, v, causal=causal)
-    dq, dk, dv = attn_bwd(q, k, v, o, do, lse, causal=causal)
+    dq, dk, dv = attn_bwd(q, k, v, o, do, lse, causal=causal, deterministic=True)
     torch.cuda.synchronize()
     hin = [t.cpu().pin_memory() for t in (q, k, v, o, do, lse)]
     hout = [torch.empty_like(t).pin_memory() for t in hin[:3]]
-    attn_bwd_host(*hin, *hout, causal=causal)
+    attn_bwd_host(*hin, *hout, causal=causal, deterministic=True)
     if N >= 8192:
         assert attn_last_launch_info()["kernel_launches"] > 3  # more than one chunk
     for name, got, ref in (("dq", hout[0], dq), ("dk", hout[1], dk), ("dv", hout[2], dv)):
         assert torch.equal(got.view(torch.int16), ref.cpu().view(torch.int16)), name
+
+
+def test_bwd_host_path_single_pass():
+    """attn_bwd_host with the single-pass default (d <= 64): dk, dv bit-identical
+    to attn_bwd on device copies, dq to bf16 rounding (fp32 adds in arrival order)."""
+    from paper_2511_02132_b200 import attn_bwd_host
+
+    q, k, v = synth.make_qkv(2, 16, 8, 4096, 56, base=37, device="cuda")
+    do = synth.make_tensor("q", 2, 16, 4096, 56, base=38, device="cuda")
+    o, lse = attn_fwd_lse(q, k, v, causal=True)
+    dq, dk, dv = attn_bwd(q, k, v, o, do, lse, causal=True)
+    torch.cuda.synchronize()
+    hin = [t.cpu().pin_memory() for t in (q, k, v, o, do, lse)]
+    hout = [torch.empty_like(t).pin_memory() for t in hin[:3]]
+    attn_bwd_host(*hin, *hout, causal=True)
+    assert torch.equal(hout[1].view(torch.int16), dk.cpu().view(torch.int16))
+    assert torch.equal(hout[2].view(torch.int16), dv.cpu().view(torch.int16))
+    dqd = (hout[0].float() - dq.cpu().float()).abs()
+    assert dqd.max().item() <= 2.0 ** -7 * max(1.0, dq.float().abs().max().item())
