@@ -1,6 +1,6 @@
 """Small launches for compute-sanitizer (memcheck / synccheck): every mapping,
 causal and not, ragged N, padded d, GQA; the CTA-pair cluster forward; the
-backward kernels."""
+backward kernels (single-pass and two-pass)."""
 import sys
 
 import torch
@@ -17,6 +17,7 @@ for (B, Hq, Hkv, N, d, causal) in [(1, 2, 2, 256, 128, False), (2, 4, 2, 300, 64
         attn_fwd(q, k, v, causal=causal, mapping=m, cluster=True)
     o, lse = attn_fwd_lse(q, k, v, causal=causal)
     do = synth.make_tensor("q", B, Hq, N, d, base=9, device="cuda")
-    attn_bwd(q, k, v, o, do, lse, causal=causal)
+    attn_bwd(q, k, v, o, do, lse, causal=causal)                      # single-pass for d <= 64
+    attn_bwd(q, k, v, o, do, lse, causal=causal, deterministic=True)  # two-pass
 torch.cuda.synchronize()
 print("sanitize run done")
