@@ -165,3 +165,73 @@ def attention_bwd(q, k, v, dout, causal: bool = False, scale: float | None = Non
     if rc != 0:
         raise ValueError(f"oracle_attn_bwd failed ({rc})")
     return dq, dk, dv, lse
+
+
+def _f64(a, code):
+    """fp64 values of an _as_np array (bf16 bit patterns widened exactly)."""
+    if code == 0:
+        return (a.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    return a.astype(np.float64)
+
+
+def attention_bwd_rows(q, k, v, dout, b: int, g: int, q_rows, k_rows, causal: bool = False,
+                       scale: float | None = None, chunk: int = 1024):
+    """fp64 gradient ROWS of batch item b and KV head g per eq:ba,
+    for sequences too long for attention_bwd's O(N^2) memory:
+      dq[hh, r] = dq[b, g*G + hh, q_rows[r], :] for every query head of group g,
+      dk[r], dv[r] = dk[b, g, k_rows[r], :], dv[b, g, k_rows[r], :].
+    Step by step (numpy, not the C oracle), for each query head h of the group:
+      1. over ALL query rows i, in chunks of `chunk` rows: s_ij = scale q_i.k_j
+         (masked j > i when causal), lse_i = log sum_j exp(s_ij),
+         o_i = sum_j exp(s_ij - lse_i) v_j, D_i = dO_i . o_i;
+      2. P_ij = exp(s_ij - lse_i), dP_ij = dO_i . v_j, dS_ij = P_ij (dP_ij - D_i);
+         dq_i = scale sum_j dS_ij k_j (sampled i);
+         dv_j += sum_i P_ij dO_i,  dk_j += scale sum_i dS_ij q_i (sampled j;
+         summed over the group's query heads)."""
+    qa, ka, va, code, (B, Hq, Hkv, N, d) = _prep(q, k, v)
+    da, cd = _as_np(dout)
+    if cd != code or da.shape != qa.shape:
+        raise ValueError("dout must match q in shape and element type")
+    if scale is None:
+        scale = 1.0 / float(np.sqrt(d))
+    G = Hq // Hkv
+    qr = np.asarray(q_rows, dtype=np.int64)
+    kr = np.asarray(k_rows, dtype=np.int64)
+    K = _f64(ka[b, g], code)
+    V = _f64(va[b, g], code)
+    dq = np.zeros((G, len(qr), d))
+    dk = np.zeros((len(kr), d))
+    dv = np.zeros((len(kr), d))
+    idx = np.arange(N)
+    for hh in range(G):
+        h = g * G + hh
+        Q = _f64(qa[b, h], code)
+        dO = _f64(da[b, h], cd)
+        lse = np.empty(N)
+        Dv = np.empty(N)
+        for c0 in range(0, N, chunk):  # step 1: row statistics of every query row
+            c1 = min(N, c0 + chunk)
+            s = scale * (Q[c0:c1] @ K.T)
+            if causal:
+                s[idx[None, :] > idx[c0:c1, None]] = -np.inf
+            m = s.max(axis=1)
+            e = np.exp(s - m[:, None])
+            l_ = e.sum(axis=1)
+            lse[c0:c1] = m + np.log(l_)
+            Dv[c0:c1] = (dO[c0:c1] * ((e @ V) / l_[:, None])).sum(axis=1)
+        # step 2, sampled query rows: dq_i
+        s = scale * (Q[qr] @ K.T)
+        if causal:
+            s[idx[None, :] > qr[:, None]] = -np.inf
+        p = np.exp(s - lse[qr, None])
+        ds = p * (dO[qr] @ V.T - Dv[qr, None])
+        dq[hh] = scale * (ds @ K)
+        # step 2, sampled key rows: dv_j, dk_j (column j of P over all queries)
+        s = scale * (Q @ K[kr].T)
+        if causal:
+            s[kr[None, :] > idx[:, None]] = -np.inf
+        p = np.exp(s - lse[:, None])
+        dv += p.T @ dO
+        ds = p * (dO @ V[kr].T - Dv[:, None])
+        dk += scale * (ds.T @ Q)
+    return dq, dk, dv

@@ -37,3 +37,37 @@ def test_c5_full_size_sampled_rows():
     got = o[:, sel][rows[:, 0], rows[:, 1], rows[:, 2]].float().cpu().numpy()
     err = np.abs(got - ref)
     assert err.max() <= 2e-2 and err.mean() <= 2e-3, (err.max(), err.mean())
+
+
+def test_c6_backward_full_size_sampled_rows():
+    """BASELINE config 6 (DeepSeek-V3 prefill shape: 128 heads x 32K keys, d = 56,
+    causal) backward at full size as `bench.py --workload C6 --pass bwd` runs it
+    (single-pass kernel, dq reduce-added over 256 key blocks per query block):
+    sampled dq / dk / dv rows of two heads against oracle.attention_bwd_rows at
+    the R21 gradient tolerance, and the column-sum identities of
+    eq:ba over ALL key rows of those heads (sum_j dv_j = sum_i dO_i,
+    sum_j dk_j = 0)."""
+    from paper_2511_02132_b200 import attn_bwd, attn_fwd_lse
+
+    B, Hq, Hkv, N, d = 1, 128, 128, 32768, 56
+    q, k, v = synth.make_qkv(B, Hq, Hkv, N, d, base=23, device="cuda")
+    do = synth.make_tensor("q", B, Hq, N, d, base=24, device="cuda")
+    o, lse = attn_fwd_lse(q, k, v, causal=True)
+    dq, dk, dv = attn_bwd(q, k, v, o, do, lse, causal=True, mapping="swizzled_head_first")
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(5)
+    idx = np.unique(np.concatenate([[0, 1, 127, 128, N // 2, N - 129, N - 2, N - 1], rng.integers(0, N, 12)]))
+    for h in (0, 127):
+        sl = slice(h, h + 1)
+        qh, kh, vh, doh = (t[:, sl].cpu() for t in (q, k, v, do))
+        rq, rk, rv = oa.attention_bwd_rows(qh, kh, vh, doh, 0, 0, idx, idx, causal=True, scale=1.0 / math.sqrt(d))
+        for name, g, ref in (("dq", dq[0, h, idx], rq[0]), ("dk", dk[0, h, idx], rk), ("dv", dv[0, h, idx], rv)):
+            e = np.abs(g.float().cpu().numpy() - ref)
+            mx, mn = np.abs(ref).max(), np.abs(ref).mean()
+            assert e.max() <= 2e-2 * max(1.0, mx), (name, h, e.max())  # DESIGN.md reading R21
+            assert e.mean() <= 2e-3 * max(1.0, mn) + 2.0 ** -9 * mn, (name, h, e.mean())
+        # identities over every key row of the head (bf16 outputs summed in fp64)
+        sv = dv[0, h].double().sum(0).cpu().numpy()
+        np.testing.assert_allclose(sv, doh[0, 0].double().numpy().sum(0), atol=2e-3 * N ** 0.5, rtol=1e-2)
+        sk = dk[0, h].double().sum(0).cpu().numpy()
+        assert np.abs(sk).max() <= 2e-3 * N ** 0.5 * max(1.0, dk[0, h].double().abs().mean().item()), np.abs(sk).max()

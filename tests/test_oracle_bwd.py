@@ -75,3 +75,34 @@ def test_lse_closed_form_and_zero_dv_for_unseen_keys():
     np.testing.assert_allclose(lse[0, 0], np.log(np.arange(1, N + 1)), atol=1e-15, rtol=0)  # uniform rows
     # key N-1 is seen only by query N-1 with weight 1/N: dv[N-1] = dO[N-1]/N
     np.testing.assert_allclose(dv[0, 0, N - 1], do[0, 0, N - 1].numpy() / N, atol=1e-15, rtol=0)
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_rows_variant_matches_full_oracle(causal):
+    """attention_bwd_rows (numpy, chunked statistics: the full-size backward
+    parity test's checker) equals the pinned C oracle's gradients row by row,
+    GQA group sums included, with a chunk that splits the rows unevenly."""
+    from paper_2511_02132_b200 import synth
+
+    q, k, v = synth.make_qkv(2, 4, 2, 300, 24, base=5, device="cpu")
+    do = synth.make_tensor("q", 2, 4, 300, 24, base=6, device="cpu")
+    rq, rk, rv, _ = oa.attention_bwd(q, k, v, do, causal=causal)
+    qrows, krows = [0, 1, 127, 128, 299], [0, 5, 200, 299]
+    for b, g in ((0, 0), (1, 1)):
+        dq, dk, dv = oa.attention_bwd_rows(q, k, v, do, b, g, qrows, krows, causal=causal, chunk=64)
+        np.testing.assert_allclose(dq, rq[b, 2 * g:2 * g + 2][:, qrows], atol=1e-12, rtol=0)
+        np.testing.assert_allclose(dk, rk[b, g, krows], atol=1e-12, rtol=0)
+        np.testing.assert_allclose(dv, rv[b, g, krows], atol=1e-12, rtol=0)
+
+
+def test_rows_variant_column_sum_identities():
+    """Closed forms of eq:ba that hold at any size (each row of P sums to 1 and
+    sum_j P_ij dP_ij = D_i): sum_j dv_j = sum_i dO_i and sum_j dk_j = 0."""
+    from paper_2511_02132_b200 import synth
+
+    N = 96
+    q, k, v = synth.make_qkv(1, 1, 1, N, 16, base=7, device="cpu")
+    do = synth.make_tensor("q", 1, 1, N, 16, base=8, device="cpu")
+    _, dk, dv = oa.attention_bwd_rows(q, k, v, do, 0, 0, [0], np.arange(N), causal=True, chunk=40)
+    np.testing.assert_allclose(dv.sum(0), do[0, 0].double().numpy().sum(0), atol=1e-11, rtol=0)
+    np.testing.assert_allclose(dk.sum(0), 0.0, atol=1e-11)
