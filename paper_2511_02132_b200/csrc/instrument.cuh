@@ -12,7 +12,7 @@
 
 #ifdef ATTN_CYCLES
 #define ATTN_CYC_DECL() \
-  long long cyc_[8] = {0, 0, 0, 0, 0, 0, 0, 0}; \
+  long long cyc_[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}; \
   long long cyc_t_ = 0;
 #define ATTN_CYC_START() cyc_t_ = clock64();
 #define ATTN_CYC_ADD(i)                 \
@@ -34,6 +34,13 @@
     long long* cyc_out_ = reinterpret_cast<long long*>(trace) + (blockIdx.x * 8 + (warp_index)) * 8;    \
     for (int cyc_i_ = 0; cyc_i_ < 8; ++cyc_i_) cyc_out_[cyc_i_] = cyc_[cyc_i_];                          \
   }
+// forward kernel: one record of 16 counters per (CTA < 64, softmax warp); [8]
+// P stores (tcgen05.st + wait + publish), [9] O fix-up
+#define ATTN_CYC_WRITE16(trace, warp_index)                                                                \
+  if ((trace) && (threadIdx.x & 31) == 0 && blockIdx.x < 64) {                                             \
+    long long* cyc_out_ = reinterpret_cast<long long*>(trace) + (blockIdx.x * 8 + (warp_index)) * 16;   \
+    for (int cyc_i_ = 0; cyc_i_ < 16; ++cyc_i_) cyc_out_[cyc_i_] = cyc_[cyc_i_];                         \
+  }
 // pair kernel: one record of 8 counters per (CTA < 64, warp 0..11)
 #define ATTN_CYC_WRITE12(trace, warp_index)                                                                \
   if ((trace) && (threadIdx.x & 31) == 0 && blockIdx.x < 64) {                                             \
@@ -43,6 +50,7 @@
 #define ATTN_INSTRUMENTED 1
 #else
 #define ATTN_CYC_WRITE12(trace, warp_index)
+#define ATTN_CYC_WRITE16(trace, warp_index)
 #define ATTN_CYC_DECL()
 #define ATTN_CYC_START()
 #define ATTN_CYC_ADD(i)
