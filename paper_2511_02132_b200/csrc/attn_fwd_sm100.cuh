@@ -56,40 +56,12 @@ constexpr int kBlockN = 128;  // keys per K/V block
 #define ATTN_P_PARTS 2
 #endif
 constexpr int kPParts = ATTN_P_PARTS;
-// Head dim <= 64 (separate-P layout): P slices per tile (fewer MMA-warp waits)
-#ifndef ATTN_P_PARTS_D64
-#define ATTN_P_PARTS_D64 2
-#endif
 // Head dim <= 64 (plain CTAs): P gets its own TMEM columns (the 128 that
 // S0 S1 O0 O1 leave free) instead of aliasing S, so S_t(j+1) is issued as soon
 // as the softmax has loaded S_t(j) into registers and each tile's softmax runs
 // back to back instead of waiting for the PV -> S -> softmax round trip.
 #ifndef ATTN_SEP_P
 #define ATTN_SEP_P 1
-#endif
-// Head dim <= 64 (separate-P layout): the two tiles' softmax warps of an SMSP
-// take turns on the MUFU -- tile 0's exps of block j, then tile 1's, then tile
-// 0's of block j+1 -- handing an "exp token" over by named barriers, so one
-// warp's TMEM load / row max / P store runs under the other's exps instead of
-// both warps running each phase in lockstep.
-#ifndef ATTN_EXP_TOKEN_D64
-#define ATTN_EXP_TOKEN_D64 0
-#endif
-#ifndef ATTN_EXP_TOKEN_D128
-#define ATTN_EXP_TOKEN_D128 0
-#endif
-// Head dim 128: the second half of P (keys 64..127 of the block) goes to
-// SHARED memory instead of TMEM, and O += P_h1 V_h1 reads it there (SS MMA).
-// S_t(j+1) then only has to wait for O += P_h0 V_h0 (P_h0 keeps its TMEM
-// columns inside S_t), so the MMA warp issues it while the softmax is still
-// computing the exps of the second half: the per-tile softmax -> PV -> S
-// chain shrinks by the PV_h1 + S latency.  Same MMAs in the same order into
-// O, so the output is bit-identical.  Measured: the softmax's
-// S wait drops from ~850 to ~250 cycles per block, but its other phases grow
-// by as much (SMEM stores + proxy fence + more MUFU overlap), so the
-// throughput is unchanged to -1%: opt-in.
-#ifndef ATTN_PH1_SMEM
-#define ATTN_PH1_SMEM 0
 #endif
 // softmax warps per (tile, TMEM lane quarter): each handles kBlockN / kSplit
 // columns of its 32 rows, so two warps share each SMSP's MUFU per tile.
@@ -142,12 +114,7 @@ struct Cfg {
   static constexpr int kStages = (D == 128) ? ATTN_KV_STAGES : ATTN_KV_STAGES_D64;  // K/V ring slots
   static constexpr int kOffQ = 0;
   static constexpr int kOffKV = 2 * kQTileBytes;
-  // D = 128 with ATTN_PH1_SMEM: P_h1 of both tiles (128 rows x 64 keys bf16,
-  // 128B-swizzled K-major A operands, 16 KB each) after the K/V ring
-  static constexpr bool kPh1 = ATTN_PH1_SMEM && D == 128;
-  static constexpr int kPh1Bytes = kBlockM * 64 * 2;
-  static constexpr int kOffPh1 = kOffKV + kStages * kKVBytes;
-  static constexpr int kOffCtrl = kOffPh1 + (kPh1 ? 2 * kPh1Bytes : 0);
+  static constexpr int kOffCtrl = kOffKV + kStages * kKVBytes;
   static constexpr int kCtrlBytes = (kSplit == 1) ? 1024 : 8192;
   static constexpr int kSmemBytes = kOffCtrl + kCtrlBytes + 1024;  // + alignment slack
   // TMEM columns: S_t at 128*t, O_t at 256 + D*t
@@ -195,7 +162,6 @@ struct __align__(16) Ctrl {
   uint64_t o_ready[2];
   uint64_t s_free[2];       // separate-P layout: softmax loaded S_t -> MMA may overwrite it
   uint64_t p_free[2];       // separate-P layout: PV_t done reading P_t (and adding into O_t)
-  uint64_t ph1_free[2];     // P_h1 in SMEM: O_t += P_h1 V_h1 done (SMEM slot free, O_t complete)
   int4 entry[kSchedRing];  // (b, h, u, valid)
   uint32_t tmem_base;
 };
@@ -376,11 +342,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   static_assert(kCl == 1 || kCl == 2, "cluster size 1 or 2");
   constexpr bool kSepP = ATTN_SEP_P && D <= 64 && kCl == 1;
   static_assert(!kSepP || 256 + 2 * D + 128 <= kTmemCols, "separate P does not fit in TMEM");
-  constexpr int kPP = kSepP ? ATTN_P_PARTS_D64 : kPParts;  // P slices the softmax publishes per block
-  constexpr bool kPh1 = C::kPh1 && !kSepP;  // P_h1 through SMEM (D = 128)
-  static_assert(!kPh1 || kPP == 2, "P_h1 in SMEM needs two P slices");
-  [[maybe_unused]] uint8_t* ph1_smem = smem + C::kOffPh1;
-  static_assert(kPP == 1 || kPP == 2 || kPP == 4, "P slices: 1, 2 or 4");
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t crank = (kCl > 1) ? ptx::cluster_ctarank() : 0u;
@@ -400,12 +361,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&ctrl->s_ready[i], 1);
-      for (int h = 0; h < kPP; ++h)
+      for (int h = 0; h < kPParts; ++h)
         ptx::mbar_init(&ctrl->p_ready[i][h], 4 * kSplit);  // one arrive per softmax warp of the tile
       ptx::mbar_init(&ctrl->o_ready[i], 1);
       ptx::mbar_init(&ctrl->s_free[i], 4 * kSplit);
       ptx::mbar_init(&ctrl->p_free[i], 1);
-      ptx::mbar_init(&ctrl->ph1_free[i], 1);
     }
     ptx::fence_barrier_init();
   }
@@ -581,19 +541,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t d_tmem = tmem + C::col_o(t);
       const uint32_t a_tmem = tmem + (kSepP ? C::col_p(t) : C::col_s(t));
 #pragma unroll
-      for (int k = h * (8 / kPP); k < (h + 1) * (8 / kPP); ++k)
+      for (int k = h * (8 / kPParts); k < (h + 1) * (8 / kPParts); ++k)
         ptx::mma_ts(d_tmem, a_tmem + k * 8, dv + (uint64_t)((k * 16 * 128) >> 4), idesc_o,
                     (acc || k > 0) ? 1u : 0u);
-    };
-    // O_t += P_h1 V_h1 with P_h1 from SMEM (SS): K steps 4..7 of the block
-    [[maybe_unused]] const uint64_t dph1 = ptx::smem_desc_sw128(ptx::smem_u32(ph1_smem), 16, 1024);
-    auto issue_pv_h1_smem = [&](int t, int slot) {
-      const uint64_t dv = dv0 + (uint64_t)((slot * C::kKVBytes) >> 4);
-      const uint64_t da = dph1 + (uint64_t)((t * C::kPh1Bytes) >> 4);
-      const uint32_t d_tmem = tmem + C::col_o(t);
-#pragma unroll
-      for (int k = 4; k < 8; ++k)
-        ptx::mma_ss(d_tmem, da + (uint64_t)(((k & 3) * 32) >> 4), dv + (uint64_t)((k * 16 * 128) >> 4), idesc_o, 1u);
     };
     auto take_slot = [&]() {
       const int s = kv_stage;
@@ -678,7 +628,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (j < nt) {
               const uint32_t ph = (t == 0) ? p_phase0 : p_phase1;
 #pragma unroll
-              for (int h = 0; h < kPP; ++h) {
+              for (int h = 0; h < kPParts; ++h) {
                 ptx::mbar_wait(&ctrl->p_ready[t][h], ph);
                 ptx::tc_fence_after();
                 if (ptx::elect_one_sync()) issue_pv_half(t, sV, j > 0, h);
@@ -721,48 +671,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int nt = (t == 0) ? n0 : n1;
           if (j < nt) {
             const uint32_t ph = (t == 0) ? p_phase0 : p_phase1;
-            if constexpr (kPh1) {
-              // [P_h0] O += P_h0 V_h0 (TMEM), S_t(j+1) over S_t (P_h0 consumed
-              // first: in-order), [P_h1] O += P_h1 V_h1 (SMEM)
-              ptx::mbar_wait(&ctrl->p_ready[t][0], ph);
-              ptx::tc_fence_after();
-              if (ptx::elect_one_sync()) {
-                issue_pv_half(t, sV, j > 0, 0);
-                if (j + 1 < nt) {
-                  issue_s(t, sK);
-                  ptx::mma_commit(&ctrl->s_ready[t]);
-                }
-              }
-              __syncwarp();
-              ptx::mbar_wait(&ctrl->p_ready[t][1], ph);
-              ptx::tc_fence_after();
-              if (ptx::elect_one_sync()) {
-                issue_pv_h1_smem(t, sV);
-                ptx::mma_commit(j + 1 < nt ? &ctrl->ph1_free[t] : &ctrl->o_ready[t]);
-              }
-              __syncwarp();
-              if (t == 0) p_phase0 ^= 1; else p_phase1 ^= 1;
-              continue;
-            }
 #pragma unroll
-            for (int h = 0; h < kPP; ++h) {
+            for (int h = 0; h < kPParts; ++h) {
               ptx::mbar_wait(&ctrl->p_ready[t][h], ph);
               ptx::tc_fence_after();
               if (ptx::elect_one_sync()) issue_pv_half(t, sV, j > 0, h);
-#ifdef ATTN_ABL_EARLY_S  // timing ablation only (wrong results): S(j+1) between the two PV halves
-              if (h == 0 && j + 1 < nt && ptx::elect_one_sync()) {
-                issue_s(t, sK);
-                ptx::mma_commit(&ctrl->s_ready[t]);
-              }
-#endif
               __syncwarp();
             }
             if (t == 0) p_phase0 ^= 1; else p_phase1 ^= 1;
             if (ptx::elect_one_sync()) {
-#ifdef ATTN_ABL_EARLY_S
-              if (j + 1 < nt) {
-              } else
-#endif
               if (j + 1 < nt) {
                 issue_s(t, sK);
                 ptx::mma_commit(&ctrl->s_ready[t]);
@@ -819,16 +736,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     SchedReader<kCl> sr;
     uint32_t s_phase = 0, o_phase = 0, gblk = 0;
     ATTN_CYC_DECL()
-    [[maybe_unused]] uint32_t pf_phase = 0, ph1_phase = 0;
-    // exp token (separate-P layout): barrier 1 + 2*quarter hands it to tile 0,
-    // 2 + 2*quarter to tile 1; tile 1 holds it first-released (one arrive up
-    // front), so tile 0 starts.  Taken only on the key blocks both tiles of
-    // the unit have (causal: tile 1 has one more).
-    constexpr bool kToken = kSplit == 1 && ((kSepP && ATTN_EXP_TOKEN_D64) || (kPh1 && ATTN_EXP_TOKEN_D128));
-    [[maybe_unused]] const uint32_t tok_mine = 1 + 2 * quarter + t, tok_other = 2 + 2 * quarter - t;
-    if constexpr (kToken) {
-      if (t == 1) ptx::named_bar_arrive(tok_other, 64);
-    }
+    [[maybe_unused]] uint32_t pf_phase = 0;
     while (true) {
       const int4 e = sr.next(ctrl, false);
       __syncwarp();
@@ -840,7 +748,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (u >= 0) unit_blocks<kCausal>(u, p.nblk, n0, n1);
       const int nt = (t == 0) ? n0 : n1;
       if (nt == 0) continue;
-      [[maybe_unused]] const int n_common = n0 < n1 ? n0 : n1;  // key blocks both tiles have
       const int qb = 2 * u + t;
       // keys of the last key block that exist (ragged N): local key k < tail_keys
       const int last_blk = p.nblk - 1;
@@ -859,7 +766,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&ctrl->s_free[t]);
           }
-          for (int h = 0; h < kPP; ++h) {
+          for (int h = 0; h < kPParts; ++h) {
             if (kSepP && h == 0 && j > 0) {
               ptx::mbar_wait(&ctrl->p_free[t], pf_phase);
               pf_phase ^= 1;
@@ -874,12 +781,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
 #endif
         uint32_t r[kCols];
-#ifdef ATTN_ABL_NOLD  // timing ablation only (wrong results): S loaded on the first block alone
-        if (j > 0) {
-#pragma unroll
-          for (int k = 0; k < kCols; ++k) r[k] = __float_as_uint(m + 0.001f * (float)k);
-        } else
-#endif
         if constexpr (kCols == 128) ptx::tmem_ld128(trow + colS, r);
         else ptx::tmem_ld64(trow + colS, r);
         if constexpr (kSepP) {  // S_t is in registers: the MMA warp may compute S_t(j+1) over it
@@ -909,9 +810,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             mq[g4] = fmaxf(mq[g4], fmaxf(__uint_as_float(r[k + 2 * g4]), __uint_as_float(r[k + 2 * g4 + 1])));
         }
         float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
-#ifdef ATTN_ABL_NOMAX  // timing ablation only (wrong results): the row max of the first block alone
-        if (j > 0) mx = m;
-#endif
         if constexpr (kSplit == 2) {
           sred->red[t][quarter][hf][gblk & 1][lane] = mx;
           ptx::named_bar_sync(bar_id, 64);
@@ -944,20 +842,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::tmem_st32(trow + colO + cc, o);
           }
         };
-        [[maybe_unused]] bool ph1_waited = false;
-        if constexpr (kPh1) {
-          // O_t += P_h1 V_h1 of block j-1 follows S_t(j) in the MMA stream:
-          // wait for it before rescaling O_t (and, below, before P_h1 reuses its SMEM)
-          if (any_rescale) {
-            ptx::mbar_wait(&ctrl->ph1_free[t], ph1_phase);
-            ph1_phase ^= 1;
-            ph1_waited = true;
-            ptx::tc_fence_after();
-            fixup();
-          }
-        } else if (!kSepP && any_rescale) {
-          fixup();
-        }
+        if (!kSepP && any_rescale) fixup();
         const float neg = -m_use * c;
         // P = exp2(S c - m c) on (even, odd) pairs with packed f32x2 math:
         // MUFU.EX2 for most pairs, the FMA-pipe polynomial for every
@@ -965,16 +850,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         // core starts O += P V on the first half while the second is computed.
         float2 sq[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                         make_float2(0.f, 0.f)};
-        [[maybe_unused]] const bool tok = kToken && j < n_common;
         auto exp_block = [&](auto mask_tag) {
-        if constexpr (kToken) {
-          if (tok) ptx::named_bar_sync(tok_mine, 64);
-          ATTN_CYC_ADD(4);  // the token wait counts with the p_free wait
-        }
 #pragma unroll
-        for (int h = 0; h < kPP; ++h) {
+        for (int h = 0; h < kPParts; ++h) {
 #pragma unroll
-          for (int k = h * kCols / kPP; k < (h + 1) * kCols / kPP; k += 2) {
+          for (int k = h * kCols / kPParts; k < (h + 1) * kCols / kPParts; k += 2) {
             const float2 x = ptx::ffma2(make_float2(__uint_as_float(r[k]), __uint_as_float(r[k + 1])), c, neg);
             float2 pr;
             constexpr int kEP = emu_period<D>();
@@ -1000,9 +880,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             if constexpr (!kOnesL) sq[(k >> 1) & 3] = ptx::fadd2(sq[(k >> 1) & 3], pr);
             r[k >> 1] = ptx::pack_bf16(pr.x, pr.y);
           }
-          if constexpr (kToken) {
-            if (tok && h == kPP - 1) ptx::named_bar_arrive(tok_other, 64);  // last exp issued
-          }
           ATTN_CYC_ADD(3);
           if constexpr (kSepP) {
             if (h == 0 && j > 0) {  // PV_t(j-1) has finished reading P_t and adding into O_t
@@ -1014,33 +891,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               ATTN_CYC_ADD(9);
             }
           }
-          if constexpr (kPh1) {
-            if (h == 1) {  // P_h1 -> SMEM (row `row`, 128 B, 128B-swizzled 16-byte chunks), A operand of the SS PV
-              if (j > 0 && !ph1_waited) {
-                ptx::mbar_wait(&ctrl->ph1_free[t], ph1_phase);
-                ph1_phase ^= 1;
-              }
-              ATTN_CYC_ADD(4);
-              uint8_t* prow = ph1_smem + t * C::kPh1Bytes + row * 128;
-#pragma unroll
-              for (int cc = 0; cc < 8; ++cc)
-                *reinterpret_cast<uint4*>(prow + ((cc ^ (row & 7)) * 16)) =
-                    make_uint4(r[32 + 4 * cc], r[33 + 4 * cc], r[34 + 4 * cc], r[35 + 4 * cc]);
-              ATTN_CYC_ADD(10);
-              ptx::fence_proxy_async_smem();  // generic SMEM writes -> visible to the tensor core
-              ATTN_CYC_ADD(11);
-              __syncwarp();
-              if (lane == 0) ptx::mbar_arrive(&ctrl->p_ready[t][1]);
-              ATTN_CYC_ADD(8);
-              continue;
-            }
-          }
-          constexpr int kPc = kCols / kPP / 2;  // packed P columns per slice
-#ifdef ATTN_ABL_NOST  // timing ablation only (wrong results): P is not stored
-          if (gblk == 0xffffffffu) ptx::tmem_st32(trow + colP + h * 32, r + h * 32); else
-#endif
-          if constexpr (kPc == 64) ptx::tmem_st64(trow + colP, r);
-          else if constexpr (kPc == 32) ptx::tmem_st32(trow + colP + h * 32, r + h * 32);
+          constexpr int kPc = kCols / kPParts / 2;  // packed P columns per slice
+          if constexpr (kPc == 32) ptx::tmem_st32(trow + colP + h * 32, r + h * 32);
           else ptx::tmem_st16(trow + colP + h * 16, r + h * 16);
           ptx::tmem_wait_st();
           ptx::tc_fence_before();
@@ -1104,9 +956,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       ptx::tc_fence_before();
       ATTN_CYC_ADD(5);
-    }
-    if constexpr (kToken) {
-      if (t == 0) ptx::named_bar_sync(tok_mine, 64);  // tile 1's last release
     }
     ATTN_CYC_WRITE16(p.trace, warp - 4)
   } else {
