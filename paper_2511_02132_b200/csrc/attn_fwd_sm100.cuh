@@ -587,7 +587,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         // tell the softmax when P_t may be overwritten and O_t rescaled / read.
         ptx::mbar_wait(&ctrl->q_full, q_phase);
         q_phase ^= 1;
-        auto issue_s_sep = [&](int t, int slot) {
+        // S_t(j+1) once the softmax holds S_t(j) (s_free; not before a tile's
+        // first block).  Each elected group also carries the commits and ring
+        // releases that follow its MMAs in the stream (fewer elect / branch
+        // round trips in this warp, whose own loop bounds the pipeline at
+        // d <= 64: DESIGN.md section 6).
+        auto issue_s_sep = [&](int t, int slot, bool last, bool q_done) {
           int& used = (t == 0) ? s_used0 : s_used1;
           uint32_t& sfp = (t == 0) ? sf_phase0 : sf_phase1;
           if (used) {
@@ -599,29 +604,26 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (ptx::elect_one_sync()) {
             issue_s(t, slot);
             ptx::mma_commit(&ctrl->s_ready[t]);
+            if (last) {
+              kv_release(slot);
+              if (q_done) ptx::mma_commit(&ctrl->q_empty);
+            }
           }
           __syncwarp();
         };
         int sK = take_slot();
-        if (n0 > 0) issue_s_sep(0, sK);
-        if (n1 > 0) issue_s_sep(1, sK);
-        if (ptx::elect_one_sync()) {
-          kv_release(sK);
-          if (n == 1) ptx::mma_commit(&ctrl->q_empty);
-        }
-        __syncwarp();
+        // n >= 1, n0 >= 1; tile 1 absent when n1 == 0
+        issue_s_sep(0, sK, n1 == 0, n == 1);
+        if (n1 > 0) issue_s_sep(1, sK, true, n == 1);
         for (int j = 0; j < n; ++j) {
           if (j + 1 < n) {
             sK = take_slot();
-            if (j + 1 < n0) issue_s_sep(0, sK);
-            if (j + 1 < n1) issue_s_sep(1, sK);
-            if (ptx::elect_one_sync()) {
-              kv_release(sK);
-              if (j + 2 == n) ptx::mma_commit(&ctrl->q_empty);
-            }
-            __syncwarp();
+            const bool a0 = j + 1 < n0, a1 = j + 1 < n1;  // a0 || a1
+            if (a0) issue_s_sep(0, sK, !a1, j + 2 == n);
+            if (a1) issue_s_sep(1, sK, true, j + 2 == n);
           }
           const int sV = take_slot();
+          const bool v1 = j < n1;  // tile 1 uses V(j); tile 0 does whenever tile 1 does not
 #pragma unroll
           for (int t = 0; t < 2; ++t) {
             const int nt = (t == 0) ? n0 : n1;
@@ -631,16 +633,18 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int h = 0; h < kPParts; ++h) {
                 ptx::mbar_wait(&ctrl->p_ready[t][h], ph);
                 ptx::tc_fence_after();
-                if (ptx::elect_one_sync()) issue_pv_half(t, sV, j > 0, h);
+                if (ptx::elect_one_sync()) {
+                  issue_pv_half(t, sV, j > 0, h);
+                  if (h == kPParts - 1) {
+                    ptx::mma_commit(j + 1 < nt ? &ctrl->p_free[t] : &ctrl->o_ready[t]);
+                    if (t == 1 || !v1) kv_release(sV);
+                  }
+                }
                 __syncwarp();
               }
               if (t == 0) p_phase0 ^= 1; else p_phase1 ^= 1;
-              if (ptx::elect_one_sync()) ptx::mma_commit(j + 1 < nt ? &ctrl->p_free[t] : &ctrl->o_ready[t]);
-              __syncwarp();
             }
           }
-          if (ptx::elect_one_sync()) kv_release(sV);
-          __syncwarp();
         }
         continue;
       }
