@@ -675,33 +675,36 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int nt = (t == 0) ? n0 : n1;
           if (j < nt) {
             const uint32_t ph = (t == 0) ? p_phase0 : p_phase1;
+            // the last slice's group also issues S_t(j+1) (or commits O_t) and,
+            // for the last tile using this block, releases the ring slots
+            const bool last_tile = (t == 1) || (j >= n1);
 #pragma unroll
             for (int h = 0; h < kPParts; ++h) {
               ptx::mbar_wait(&ctrl->p_ready[t][h], ph);
               ptx::tc_fence_after();
-              if (ptx::elect_one_sync()) issue_pv_half(t, sV, j > 0, h);
+              if (ptx::elect_one_sync()) {
+                issue_pv_half(t, sV, j > 0, h);
+                if (h == kPParts - 1) {
+                  if (j + 1 < nt) {
+                    issue_s(t, sK);
+                    ptx::mma_commit(&ctrl->s_ready[t]);
+                  } else {
+                    ptx::mma_commit(&ctrl->o_ready[t]);
+                  }
+                  if (last_tile) {
+                    kv_release(sV);
+                    if (nxt) {
+                      kv_release(sK);
+                      if (j + 2 == n) ptx::mma_commit(&ctrl->q_empty);
+                    }
+                  }
+                }
+              }
               __syncwarp();
             }
             if (t == 0) p_phase0 ^= 1; else p_phase1 ^= 1;
-            if (ptx::elect_one_sync()) {
-              if (j + 1 < nt) {
-                issue_s(t, sK);
-                ptx::mma_commit(&ctrl->s_ready[t]);
-              } else {
-                ptx::mma_commit(&ctrl->o_ready[t]);
-              }
-            }
-            __syncwarp();
           }
         }
-        if (ptx::elect_one_sync()) {
-          kv_release(sV);
-          if (nxt) {
-            kv_release(sK);
-            if (j + 2 == n) ptx::mma_commit(&ctrl->q_empty);
-          }
-        }
-        __syncwarp();
       }
       if constexpr (kCl > 1) {
         for (int j = 0; j < extra_blocks; ++j) {

@@ -1,4 +1,6 @@
 set -u
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/exp16_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/exp16_pytest.log
-timeout 900 python bench.py --workload C6 > gpurun_out/exp16_bench_C6.json 2> gpurun_out/exp16_bench_C6.err
+rm -f /tmp/vref.pt
+ATTN_NUMA_LIB=paper_2511_02132_b200/lib/var/base.so VARIANT_REF=/tmp/vref.pt timeout 300 python scripts/variant_check.py > gpurun_out/exp17_check.log 2>&1
+ATTN_NUMA_LIB=paper_2511_02132_b200/lib/var2/grp128.so VARIANT_REF=/tmp/vref.pt timeout 300 python scripts/variant_check.py >> gpurun_out/exp17_check.log 2>&1
+for r in 1 2 3; do for v in var/base var2/grp128; do echo "== $v" ; ATTN_NUMA_LIB=paper_2511_02132_b200/lib/$v.so timeout 300 python scripts/quick_bench.py --configs C2,C3 --reps 5 --maps swizzled_head_first 2>&1 | grep -v '^{'; done; done > gpurun_out/exp17_bench.log 2>&1
