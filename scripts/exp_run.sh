@@ -1,3 +1,3 @@
 set -u
 mkdir -p gpurun_out
-timeout 900 python bench.py --workload C3 --no-cpu-baseline > gpurun_out/exp22_C3.json 2> gpurun_out/exp22_C3.err
+timeout 600 python -m pytest tests/test_gpu_graph.py -q -x > gpurun_out/exp23_graph.log 2>&1; echo "rc=$?" >> gpurun_out/exp23_graph.log
