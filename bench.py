@@ -90,6 +90,19 @@ def load_peaks():
         return 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
 
 
+def mapping_rounds(ms_step: float):
+    """by_mapping protocol for a step of ms_step ms: (timed steps per chunk,
+    untimed settle steps before each chunk, interleaved rounds).  A chunk is
+    ~300 ms of back-to-back steps (at least one), the settle half as long (at
+    least one step), and the rounds give ~2 s of timed steps per variant
+    (3..50 rounds)."""
+    ms = max(ms_step, 1e-3)
+    chunk = max(1, int(round(300.0 / ms)))
+    settle = max(1, chunk // 2)
+    rounds = max(3, min(50, int(round(2000.0 / (chunk * ms)))))
+    return chunk, settle, rounds
+
+
 def variant_key(mapping, cluster, order="ascending"):
     return f"{mapping}{'+cluster' if cluster else ''}{'' if order == 'ascending' else '+' + order}"
 
@@ -350,9 +363,7 @@ def run_ours(a):
     # steps per variant (~300 ms), the first half untimed (settle), the second
     # half timed as one event pair; by_mapping = median over ~6 rounds of the
     # per-step chunk times (about 2 s timed per variant).
-    chunk = max(1, int(round(300.0 / max(ms_step, 1e-3))))
-    settle = max(1, chunk // 2)
-    rounds = max(3, min(50, int(round(2000.0 / (chunk * max(ms_step, 1e-3))))))
+    chunk, settle, rounds = mapping_rounds(ms_step)
     per_var = {v: [] for v in variants}
     for v in variants:  # one untimed step each (descriptors, first-touch)
         step(0, v)

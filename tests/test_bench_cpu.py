@@ -69,3 +69,16 @@ def test_reference_arm_runs_on_cpu():
     assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"] == {"value": line["value"], "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
     assert line["steps"] == 2 and line["warmup"] == 3 and line["higher_is_better"] is True
+
+
+def test_mapping_rounds_protocol():
+    # C5 (~463 ms per step): one timed step after one settle step, ~2 s timed
+    assert bench.mapping_rounds(463.0) == (1, 1, 4)
+    # C3 (~30 ms): 10-step chunks after 5 settle steps, 7 rounds
+    assert bench.mapping_rounds(30.0) == (10, 5, 7)
+    # C2 (~0.82 ms): ~300 ms chunks
+    chunk, settle, rounds = bench.mapping_rounds(0.82)
+    assert chunk == 366 and settle == 183 and rounds == 7
+    for ms in (0.01, 1.0, 50.0, 5000.0):
+        c, st, r = bench.mapping_rounds(ms)
+        assert c >= 1 and st >= 1 and 3 <= r <= 50
