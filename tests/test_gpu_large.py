@@ -71,3 +71,29 @@ def test_c6_backward_full_size_sampled_rows():
         np.testing.assert_allclose(sv, doh[0, 0].double().numpy().sum(0), atol=2e-3 * N ** 0.5, rtol=1e-2)
         sk = dk[0, h].double().sum(0).cpu().numpy()
         assert np.abs(sk).max() <= 2e-3 * N ** 0.5 * max(1.0, dk[0, h].double().abs().mean().item()), np.abs(sk).max()
+
+
+@pytest.mark.parametrize("causal", [True, False])
+def test_million_token_sequence_sampled_rows(causal):
+    """Maximum-length case: N = 2^20 + 77 keys (ragged last block; 8193 key
+    blocks, 4097 units per head, 64-bit row offsets) on a GQA head pair,
+    every mapping bit-identical, sampled rows (first, block edges, the ragged
+    tail, random) vs the fp64 oracle at the north-star tolerance."""
+    B, Hq, Hkv, N, d = 1, 2, 1, (1 << 20) + 77, 128
+    q, k, v = synth.make_qkv(B, Hq, Hkv, N, d, base=31, device="cuda")
+    outs = []
+    for m in ("block_first", "swizzled_head_first"):
+        o = torch.full_like(q, float("nan"))
+        attn_fwd(q, k, v, o, causal=causal, mapping=m)
+        torch.cuda.synchronize()
+        outs.append(o)
+    assert torch.equal(outs[0].view(torch.int16), outs[1].view(torch.int16))
+    o = outs[1]
+    assert not torch.isnan(o[:, :, ::97].float()).any() and not torch.isnan(o[:, :, -200:].float()).any()
+    rng = np.random.default_rng(5)
+    idx = np.concatenate([[0, 1, 127, 128, N // 2, N - 78, N - 77, N - 2, N - 1], rng.integers(0, N, 7)])
+    rows = np.array([[0, h, i] for h in range(Hq) for i in idx], dtype=np.int64)
+    ref = oa.attention_rows(q.cpu(), k.cpu(), v.cpu(), rows, causal=causal, scale=1.0 / math.sqrt(d))
+    got = o[rows[:, 0], rows[:, 1], rows[:, 2]].float().cpu().numpy()
+    err = np.abs(got - ref)
+    assert err.max() <= 2e-2 and err.mean() <= 2e-3, (err.max(), err.mean())
