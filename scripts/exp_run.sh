@@ -1,3 +1,5 @@
 set -u
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_large.py -q -x -k million > gpurun_out/exp24_large.log 2>&1; echo "rc=$?" >> gpurun_out/exp24_large.log
+timeout 600 python scripts/soak.py 300 > gpurun_out/soak_final.log 2>&1; echo "rc=$?" >> gpurun_out/soak_final.log
+timeout 1200 compute-sanitizer --tool memcheck python scripts/sanitize_small.py > gpurun_out/san_mem_final.log 2>&1; echo "rc=$?" >> gpurun_out/san_mem_final.log
+timeout 1200 compute-sanitizer --tool synccheck python scripts/sanitize_small.py > gpurun_out/san_sync_final.log 2>&1; echo "rc=$?" >> gpurun_out/san_sync_final.log
