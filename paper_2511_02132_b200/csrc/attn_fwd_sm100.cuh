@@ -63,14 +63,6 @@ constexpr int kPParts = ATTN_P_PARTS;
 #ifndef ATTN_SEP_P
 #define ATTN_SEP_P 1
 #endif
-// Head dim 128 (plain CTAs): ONE S buffer in TMEM shared by the two tiles
-// (S_0(j), S_1(j), S_0(j+1), ... each issued once the other tile has loaded
-// the previous one into registers) so that P_0, P_1 get their own columns:
-// S [0,128) | P_0 [128,192) | P_1 [192,256) | O_0 [256,384) | O_1 [384,512).
-// Then no S waits for an O += P V (the separate-P pipeline of D <= 64).
-#ifndef ATTN_SHARED_S
-#define ATTN_SHARED_S 0
-#endif
 // softmax warps per (tile, TMEM lane quarter): each handles kBlockN / kSplit
 // columns of its 32 rows, so two warps share each SMSP's MUFU per tile.
 constexpr int kSplit = ATTN_SPLIT;
@@ -126,7 +118,6 @@ struct Cfg {
   static constexpr int kCtrlBytes = (kSplit == 1) ? 1024 : 8192;
   static constexpr int kSmemBytes = kOffCtrl + kCtrlBytes + 1024;  // + alignment slack
   // TMEM columns: S_t at 128*t, O_t at 256 + D*t
-  static constexpr bool kSharedS = ATTN_SHARED_S && D == 128;
   static __device__ __forceinline__ uint32_t col_s(int t) { return 128u * t; }
   static __device__ __forceinline__ uint32_t col_o(int t) { return 256u + (uint32_t)D * t; }
   // separate-P layout (D <= 64): P_t (bf16 pairs, 64 columns) after O1
@@ -349,12 +340,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   static_assert(C::kSmemBytes <= 232448, "shared memory exceeds 227 KB");
 
   static_assert(kCl == 1 || kCl == 2, "cluster size 1 or 2");
-  constexpr bool kSepP = ((ATTN_SEP_P && D <= 64) || C::kSharedS) && kCl == 1;
-  constexpr bool kShS = C::kSharedS && kCl == 1;  // one S buffer: s_free[0] serves both tiles
-  // TMEM columns of S_t and P_t (shared-S layout: S [0,128), P_t at 128 + 64 t)
-  auto col_s = [](int t) -> uint32_t { return kShS ? 0u : C::col_s(t); };
-  auto col_p = [](int t) -> uint32_t { return kShS ? 128u + 64u * (uint32_t)t : C::col_p(t); };
-  static_assert(!kSepP || kShS || 256 + 2 * D + 128 <= kTmemCols, "separate P does not fit in TMEM");
+  constexpr bool kSepP = ATTN_SEP_P && D <= 64 && kCl == 1;
+  static_assert(!kSepP || 256 + 2 * D + 128 <= kTmemCols, "separate P does not fit in TMEM");
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t crank = (kCl > 1) ? ptx::cluster_ctarank() : 0u;
@@ -539,7 +526,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto issue_s = [&](int t, int slot) {
       const uint64_t dq = dq0 + (uint64_t)((t * C::kQTileBytes) >> 4);
       const uint64_t dk = dkv0 + (uint64_t)((slot * C::kKVBytes) >> 4);
-      const uint32_t d_tmem = tmem + col_s(t);
+      const uint32_t d_tmem = tmem + C::col_s(t);
 #pragma unroll
       for (int k = 0; k < D / 16; ++k) {
         const uint32_t oq = ((k >> 2) * (kBlockM * 128) + (k & 3) * 32) >> 4;
@@ -552,7 +539,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto issue_pv_half = [&](int t, int slot, bool acc, int h) {
       const uint64_t dv = dv0 + (uint64_t)((slot * C::kKVBytes) >> 4);
       const uint32_t d_tmem = tmem + C::col_o(t);
-      const uint32_t a_tmem = tmem + (kSepP ? col_p(t) : col_s(t));
+      const uint32_t a_tmem = tmem + (kSepP ? C::col_p(t) : C::col_s(t));
 #pragma unroll
       for (int k = h * (8 / kPParts); k < (h + 1) * (8 / kPParts); ++k)
         ptx::mma_ts(d_tmem, a_tmem + k * 8, dv + (uint64_t)((k * 16 * 128) >> 4), idesc_o,
@@ -606,11 +593,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         // round trips in this warp, whose own loop bounds the pipeline at
         // d <= 64: DESIGN.md section 6).
         auto issue_s_sep = [&](int t, int slot, bool last, bool q_done) {
-          // shared S buffer: every S waits for the buffer's previous occupant
-          int& used = (t == 0 || kShS) ? s_used0 : s_used1;
-          uint32_t& sfp = (t == 0 || kShS) ? sf_phase0 : sf_phase1;
+          int& used = (t == 0) ? s_used0 : s_used1;
+          uint32_t& sfp = (t == 0) ? sf_phase0 : sf_phase1;
           if (used) {
-            ptx::mbar_wait(&ctrl->s_free[kShS ? 0 : t], sfp);
+            ptx::mbar_wait(&ctrl->s_free[t], sfp);
             sfp ^= 1;
           }
           used = 1;
@@ -625,50 +611,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           __syncwarp();
         };
-        // PV_t(j) from slot sV in kPParts slices; the last slice's group commits
-        // p_free / o_ready and, if `rel`, releases the V slot
-        auto issue_pv_sep = [&](int t, int j, int nt, int sV, bool rel) {
-          const uint32_t ph = (t == 0) ? p_phase0 : p_phase1;
-#pragma unroll
-          for (int h = 0; h < kPParts; ++h) {
-            ptx::mbar_wait(&ctrl->p_ready[t][h], ph);
-            ptx::tc_fence_after();
-            if (ptx::elect_one_sync()) {
-              issue_pv_half(t, sV, j > 0, h);
-              if (h == kPParts - 1) {
-                ptx::mma_commit(j + 1 < nt ? &ctrl->p_free[t] : &ctrl->o_ready[t]);
-                if (rel) kv_release(sV);
-              }
-            }
-            __syncwarp();
-          }
-          if (t == 0) p_phase0 ^= 1; else p_phase1 ^= 1;
-        };
-        if constexpr (kShS) {
-          // one S buffer: S_0(0), S_1(0), S_0(1), S_1(1), ... each after the
-          // other tile loaded the previous one.  Issue order per iteration j
-          // (the order the events become ready when the tiles run half a
-          // period apart): S_1(j), O_1 += P_1(j-1) V(j-1), S_0(j+1), O_0 += P_0(j) V(j).
-          // K(j) serves S_0(j) and S_1(j); V(j) serves PV_0(j) and PV_1(j).
-          const int n_s = n0 + n1;
-          int s_count = 0;
-          int sKc = take_slot(), sKn = -1, sVp = -1, sVc = -1;  // K(j), K(j+1), V(j-1), V(j)
-          issue_s_sep(0, sKc, n1 == 0, ++s_count == n_s);
-          for (int j = 0; j < n; ++j) {
-            if (j < n1) issue_s_sep(1, sKc, true, ++s_count == n_s);                 // S_1(j): last user of K(j)
-            if (j >= 1 && j - 1 < n1) issue_pv_sep(1, j - 1, n1, sVp, true);         // PV_1(j-1): last user of V(j-1)
-            if (j + 1 < n) sKn = take_slot();
-            if (j + 1 < n0) issue_s_sep(0, sKn, j + 1 >= n1, ++s_count == n_s);      // S_0(j+1)
-            sVc = take_slot();
-            if (j < n0) issue_pv_sep(0, j, n0, sVc, j >= n1);                        // PV_0(j)
-            else if (j >= n1 && ptx::elect_one_sync()) kv_release(sVc);             // (not reached: j < n)
-            __syncwarp();
-            sKc = sKn;
-            sVp = sVc;
-          }
-          if (n1 > 0 && n1 - 1 == n - 1) issue_pv_sep(1, n - 1, n1, sVp, true);      // PV_1(n-1)
-          continue;
-        }
         int sK = take_slot();
         // n >= 1, n0 >= 1; tile 1 absent when n1 == 0
         issue_s_sep(0, sK, n1 == 0, n == 1);
@@ -790,8 +732,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row = quarter * 32 + lane;     // row within the 128-row tile
     const int cbase = hf * kCols;            // first key column of this thread's slice
     const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
-    const uint32_t colS = col_s(t) + cbase;
-    const uint32_t colP = (kSepP ? col_p(t) : col_s(t)) + cbase / 2;
+    const uint32_t colS = C::col_s(t) + cbase;
+    const uint32_t colP = (kSepP ? C::col_p(t) : C::col_s(t)) + cbase / 2;
     const uint32_t colO = C::col_o(t) + hf * kOCols;
     [[maybe_unused]] const uint32_t bar_id = 1 + t * 4 + quarter;  // named barrier of the row group's warps
     const float c = p.scale_log2;
@@ -829,7 +771,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if constexpr (kSepP) {
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&ctrl->s_free[kShS ? 0 : t]);
+            if (lane == 0) ptx::mbar_arrive(&ctrl->s_free[t]);
           }
           for (int h = 0; h < kPParts; ++h) {
             if (kSepP && h == 0 && j > 0) {
@@ -851,7 +793,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (kSepP) {  // S_t is in registers: the MMA warp may compute S_t(j+1) over it
           ptx::tc_fence_before();
           __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(&ctrl->s_free[kShS ? 0 : t]);
+          if (lane == 0) ptx::mbar_arrive(&ctrl->s_free[t]);
         }
         // visible local keys are k <= lim: causal diagonal block (key <= query)
         // and/or the ragged last key block (key < N)
