@@ -850,9 +850,13 @@ int bwd_impl(const void* q, const void* k, const void* v, const void* o, const v
   float* dvec = nullptr;
   float* dq_acc = nullptr;  // fused path: fp32 [B*Hq][N][64]
   // two-pass: rowsum(dO o O) per row; fused: -lse2 / -D in blocks of 128 rows (attn_bwd_prep_kernel)
+  // two-pass: both (dQ reads D per row, dK/dV the blocks), in one allocation
   const int nblk_ws = (N + bwd::kBM - 1) / bwd::kBM;
-  const size_t vec_floats = fused ? (size_t)B * Hq * nblk_ws * 2 * bwd::kBM : rows;
+  const size_t blk_floats = (size_t)B * Hq * nblk_ws * 2 * bwd::kBM;
+  const size_t rows_pad = (rows + 63) & ~(size_t)63;  // the blocks are bulk-copied: 16-B (here 256-B) aligned
+  const size_t vec_floats = fused ? blk_floats : blk_floats + rows_pad;
   ATTN_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&dvec), vec_floats * sizeof(float), pool, stream));
+  float* vecb = fused ? dvec : dvec + rows_pad;  // the blocked (-lse2 | -D) layout
   if (fused) {
     if (cudaError_t e = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&dq_acc), rows * dpad * sizeof(float), pool,
                                                 stream);
@@ -869,7 +873,7 @@ int bwd_impl(const void* q, const void* k, const void* v, const void* o, const v
   bwd::BwdParams pq{};
   pq.B = B; pq.Hq = Hq; pq.Hkv = Hkv; pq.N = N; pq.G = Hq / Hkv; pq.nblk = nblk; pq.d_real = d;
   pq.scale = scale; pq.scale_log2 = scale * 1.4426950408889634f;
-  pq.lse = lse; pq.dvec = dvec;
+  pq.lse = lse; pq.dvec = dvec; pq.vecb = vecb;
   pq.dq = reinterpret_cast<__nv_bfloat16*>(dq);
   pq.dk = reinterpret_cast<__nv_bfloat16*>(dk);
   pq.dv = reinterpret_cast<__nv_bfloat16*>(dv);
@@ -896,19 +900,20 @@ int bwd_impl(const void* q, const void* k, const void* v, const void* o, const v
     free_ws();
     return rc;
   }
-  const long long nrows = (long long)rows;
   if (fused) {
     const long long prows = (long long)B * Hq * nblk * bwd::kBM;
     bwd::attn_bwd_prep_kernel<<<(unsigned)((prows + 7) / 8), 256, 0, stream>>>(
         reinterpret_cast<const __nv_bfloat16*>(o), reinterpret_cast<const __nv_bfloat16*>(dout), lse, dvec,
         (long long)B * Hq, N, nblk, d);
-  } else {
-    bwd::attn_bwd_dot_kernel<<<(unsigned)((nrows + 7) / 8), 256, 0, stream>>>(
-        reinterpret_cast<const __nv_bfloat16*>(o), reinterpret_cast<const __nv_bfloat16*>(dout), dvec, nrows, d);
+  } else {  // D per row (dQ kernel) and the blocked -lse2 / -D (dK/dV kernel) in one pass
+    const long long prows = (long long)B * Hq * nblk * bwd::kBM;
+    bwd::attn_bwd_prep_kernel<<<(unsigned)((prows + 7) / 8), 256, 0, stream>>>(
+        reinterpret_cast<const __nv_bfloat16*>(o), reinterpret_cast<const __nv_bfloat16*>(dout), lse, vecb,
+        (long long)B * Hq, N, nblk, d, dvec);
   }
   if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) {
     free_ws();
-    return cuda_fail(e, "attn_bwd_dot_kernel / attn_bwd_prep_kernel launch");
+    return cuda_fail(e, "attn_bwd_prep_kernel launch");
   }
   const int grid_q = std::min(st.num_sms, B * Hq * nblk), grid_kv = std::min(st.num_sms, B * Hkv * nblk);
   if (fused) {

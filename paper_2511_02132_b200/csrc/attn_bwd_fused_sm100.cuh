@@ -86,9 +86,10 @@ struct BlockWalk {
 // copy brings a block's: vec[(bh*nblk + i)*256 + r] = -lse[row]*log2(e) and
 // vec[... + 128 + r] = -rowsum(dO o O)[row] for row = i*128 + r < N, 0 past N.
 // One warp per (padded) row.
+// drow (optional): rowsum(dO o O) per row as well (the two-pass dQ kernel's input).
 __global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
                                      const float* __restrict__ lse, float* __restrict__ vec, long long bh_count, int N,
-                                     int nblk, int d) {
+                                     int nblk, int d, float* __restrict__ drow = nullptr) {
   const long long prow = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   const long long npad = (long long)nblk * kBM;
@@ -112,6 +113,7 @@ __global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, const 
     float* blk = vec + (bh * nblk + n / kBM) * (2 * kBM);
     blk[n % kBM] = -l2;
     blk[kBM + n % kBM] = -acc;
+    if (drow != nullptr && n < N) drow[bh * N + n] = acc;
   }
 }
 

@@ -8,7 +8,9 @@
 // mappings apply to the backward's work units too ("each
 // workgroup computing different row blocks of the gradients ... may share the
 // same Q, K, V, and dO tensors within the same attention head"):
-//   attn_bwd_dot_kernel   D[b,h,i] = sum_c dO * O                (bandwidth)
+//   attn_bwd_prep_kernel  D[b,h,i] = sum_c dO * O per row, and per 128-row block
+//                         the vectors -lse*log2(e), -D that the dK/dV kernel
+//                         bulk-copies with each Q_i / dO_i (bandwidth)
 //   attn_bwd_dq_kernel    unit = (b, h, 128-row query block); Q and dO copied
 //                         to TMEM once per unit; loops over key blocks:
 //                         S = Q K_j^T and dP = dO V_j^T (TS MMAs) ->
@@ -55,8 +57,10 @@ struct BCfg {
   // dynamic SMEM base is 1024-B aligned (checked in-kernel), which lets the
   // dK/dV kernel use the full 227 KB at D = 128.
   static constexpr int kOffCtrl = 0;          // BCtrl (<= 1 KB)
-  static constexpr int kOffVec = 1024;        // dKdV: staged lse2 / D (2 parities x 2 x 128 floats)
+  static constexpr int kOffVec = 1024;        // dKdV: -lse2 / -D of each ring stage's query block (kStages x 1 KB)
+  static constexpr int kVecBytes = 2 * kBM * 4;
   static constexpr int kOffA = 3072;          // resident pair (dQ: Q, dO;  dKdV: K, V)
+  static_assert(kOffVec + kStages * kVecBytes <= kOffA, "ring-stage vectors overlap the K/V tiles");
   static constexpr int kOffRing = kOffA + 2 * kTile;  // ring of streamed pairs (dQ: K, V;  dKdV: Q, dO)
   static constexpr int kOffPT = kOffRing + kStages * 2 * kTile;  // dKdV: P^T, 128 x 128 bf16 (SW128 K-major)
   static constexpr int kSmemBytesKV = kOffPT + kBM * kBM * 2;    // dK/dV kernel
@@ -72,6 +76,7 @@ struct BwdParams {
   float scale, scale_log2;
   const float* lse;    // [B][Hq][N], natural log
   const float* dvec;   // [B][Hq][N], rowsum(dO o O)
+  const float* vecb;   // two-pass dK/dV: attn_bwd_prep_kernel's blocks (-lse2 | -D per 128 query rows)
   __nv_bfloat16* dq;   // [B][Hq][N][d]
   __nv_bfloat16* dk;   // [B][Hkv][N][d]
   __nv_bfloat16* dv;   // [B][Hkv][N][d]
@@ -152,24 +157,6 @@ struct BSchedReader {
     return e;
   }
 };
-
-// ------------------------------------------------------------------ D = rowsum(dO o O)
-__global__ void attn_bwd_dot_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
-                                    float* __restrict__ dvec, long long rows, int d) {
-  const long long row = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-  const int lane = threadIdx.x & 31;
-  if (row >= rows) return;
-  const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(o + row * d);
-  const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(dout + row * d);
-  float acc = 0.f;
-  for (int c = lane; c < d / 2; c += 32) {
-    const float2 x = __bfloat1622float2(a[c]), y = __bfloat1622float2(b[c]);
-    acc = fmaf(x.x, y.x, fmaf(x.y, y.y, acc));
-  }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-  if (lane == 0) dvec[row] = acc;
-}
 
 // Causal: query block i needs key blocks 0..i;  key block j is needed by query
 // blocks j..nblk-1.  Non-causal: all blocks.
@@ -574,7 +561,7 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
           const int bh = b * p.Hq + g * p.G + hh;
           for (int i = dkdv_first_qblock<kCausal>(j); i < p.nblk; ++i) {
             ptx::mbar_wait(&ctrl->ring_empty[stage], r_phase ^ 1);
-            ptx::mbar_arrive_expect_tx(&ctrl->ring_full[stage], 2 * C::kTile);
+            ptx::mbar_arrive_expect_tx(&ctrl->ring_full[stage], 2 * C::kTile + C::kVecBytes);
             uint8_t* dst = ring + stage * 2 * C::kTile;
 #pragma unroll
             for (int c = 0; c < C::kChunks; ++c) {
@@ -582,6 +569,9 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
               ptx::tma_load_3d(dst + C::kTile + c * kBM * 128, &tm_do, &ctrl->ring_full[stage], c * 64, i * kBM, bh,
                                pol_q);
             }
+            // the block's -lse2 / -D (attn_bwd_prep_kernel) with the same barrier
+            ptx::bulk_load(smem + C::kOffVec + stage * C::kVecBytes, p.vecb + ((long long)bh * p.nblk + i) * (2 * kBM),
+                           C::kVecBytes, &ctrl->ring_full[stage], pol_q);
             if (++stage == C::kStages) { stage = 0; r_phase ^= 1; }
           }
         }
@@ -694,37 +684,22 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
     // dS^T = P^T o (dP^T - D) stored bf16 over dP^T.
     const int quarter = warp & 3, krow = quarter * 32 + lane;  // key row of the block
     const int half = (warp - 4) >> 2, q0c = half * 64;
-    const int et = threadIdx.x - 128;                           // 0..255
     const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
     const float c = p.scale_log2;
     BSchedReader sr;
     uint32_t s_phase = 0, o_phase = 0, blk = 0, pt_phase = 0;
-    float* svec = reinterpret_cast<float*>(smem + C::kOffVec);  // [parity][lse2 | D]
     while (true) {
       const int4 e = sr.next(ctrl);
       if (!e.w) break;
       const int b = e.x, g = e.y, j = e.z;
       const int kglob = j * kBM + krow;
       const int i0 = dkdv_first_qblock<kCausal>(j);
-      // lse (as log2) and D of each block's 128 queries are staged in SMEM
-      // (double-buffered by block parity); thread et stages one value, which
-      // it loads from global one block ahead so the L2 latency stays hidden
-      const int qq = et & (kBM - 1);
-      auto stage_load = [&](int hh_, int i_) -> float {
-        const long long vi = (long long)(b * p.Hq + g * p.G + hh_) * p.N + i_ * kBM;
-        if (i_ * kBM + qq >= p.N) return 0.f;
-        return et < kBM ? __ldg(p.lse + vi + qq) * 1.4426950408889634f : __ldg(p.dvec + vi + qq);
-      };
-      float staged = stage_load(0, i0);
       for (int hh = 0; hh < p.G; ++hh) {
         for (int i = i0; i < p.nblk; ++i) {
-          float* sv = svec + (blk & 1) * 2 * kBM;
-          sv[et < kBM ? qq : kBM + qq] = staged;
-          ptx::named_bar_sync(1, 256);
-          {  // prefetch the next block's value
-            const bool last_i = i + 1 == p.nblk;
-            if (!last_i || hh + 1 < p.G) staged = stage_load(last_i ? hh + 1 : hh, last_i ? i0 : i + 1);
-          }
+          // this block's -lse2 / -D: bulk-copied with Q_i, dO_i into ring stage blk % kStages
+          const int rs = (int)(blk % C::kStages);
+          ptx::mbar_wait(&ctrl->ring_full[rs], (blk / C::kStages) & 1);
+          const float* sv = reinterpret_cast<const float*>(smem + C::kOffVec + rs * C::kVecBytes);
           ++blk;
           // visible queries of this key: q >= k (causal), q < N; local query index
           int qlo = 0, qhi = kBM - 1;
@@ -746,7 +721,7 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
                 const int q = q0c + k + u;
-                const float pe = bwd_ex2(fmaf(pv[k + u], c, -lv[u]), k + u);
+                const float pe = bwd_ex2(fmaf(pv[k + u], c, lv[u]), k + u);  // lv = -lse2
                 pv[k + u] = (q >= qlo && q <= qhi) ? pe : 0.f;
               }
             }
@@ -754,10 +729,10 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
 #pragma unroll
             for (int k = 0; k < 64; k += 4) {
               const float4 l4 = *reinterpret_cast<const float4*>(sv + q0c + k);
-              pv[k] = bwd_ex2(fmaf(pv[k], c, -l4.x), k);
-              pv[k + 1] = bwd_ex2(fmaf(pv[k + 1], c, -l4.y), k + 1);
-              pv[k + 2] = bwd_ex2(fmaf(pv[k + 2], c, -l4.z), k + 2);
-              pv[k + 3] = bwd_ex2(fmaf(pv[k + 3], c, -l4.w), k + 3);
+              pv[k] = bwd_ex2(fmaf(pv[k], c, l4.x), k);
+              pv[k + 1] = bwd_ex2(fmaf(pv[k + 1], c, l4.y), k + 1);
+              pv[k + 2] = bwd_ex2(fmaf(pv[k + 2], c, l4.z), k + 2);
+              pv[k + 3] = bwd_ex2(fmaf(pv[k + 3], c, l4.w), k + 3);
             }
           }
           // P^T -> SMEM (SW128 K-major: key row krow, 16-B unit u at (u ^ (krow & 7)))
@@ -789,8 +764,8 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
               const float dvv[4] = {d4.x, d4.y, d4.z, d4.w};
 #pragma unroll
               for (int u = 0; u < 4; u += 2)
-                pd[(k + u) >> 1] = ptx::pack_bf16(pv[cc + k + u] * (__uint_as_float(dp[cc + k + u]) - dvv[u]),
-                                                  pv[cc + k + u + 1] * (__uint_as_float(dp[cc + k + u + 1]) - dvv[u + 1]));
+                pd[(k + u) >> 1] = ptx::pack_bf16(pv[cc + k + u] * (__uint_as_float(dp[cc + k + u]) + dvv[u]),  // dvv = -D
+                                                  pv[cc + k + u + 1] * (__uint_as_float(dp[cc + k + u + 1]) + dvv[u + 1]));
             }
             ptx::tmem_st16(trow + kColDP + q0c + cc / 2, pd);  // dS^T over consumed dP^T columns
           }
