@@ -424,15 +424,23 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
         // masking (causal diagonal, ragged tail, rows past N) only where some
         // lane of the warp needs it: a warp-uniform branch, no per-element
         // compare + select on the common path
+        // x = S * c - lse2, two columns per FFMA2 (the same rounding as fmaf)
+        const float nl2 = -lse2;
         if (__any_sync(0xffffffffu, lim < k0c + 63)) {
 #pragma unroll
-          for (int k = 0; k < 64; ++k) {
-            const float pe = bwd_ex2(fmaf(pv[k], c, -lse2), k);
-            pv[k] = (k0c + k <= lim) ? pe : 0.f;
+          for (int k = 0; k < 64; k += 2) {
+            const float2 x = ptx::ffma2(make_float2(pv[k], pv[k + 1]), c, nl2);
+            const float p0 = bwd_ex2(x.x, k), p1 = bwd_ex2(x.y, k + 1);
+            pv[k] = (k0c + k <= lim) ? p0 : 0.f;
+            pv[k + 1] = (k0c + k + 1 <= lim) ? p1 : 0.f;
           }
         } else {
 #pragma unroll
-          for (int k = 0; k < 64; ++k) pv[k] = bwd_ex2(fmaf(pv[k], c, -lse2), k);
+          for (int k = 0; k < 64; k += 2) {
+            const float2 x = ptx::ffma2(make_float2(pv[k], pv[k + 1]), c, nl2);
+            pv[k] = bwd_ex2(x.x, k);
+            pv[k + 1] = bwd_ex2(x.y, k + 1);
+          }
         }
         BWD_ESTAMP(j, 2);
         ptx::mbar_wait(&ctrl->dp_ready, s_phase);
@@ -446,9 +454,12 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
           for (int cc = 0; cc < 64; cc += 32) {
             uint32_t pk[16];
 #pragma unroll
-            for (int k = 0; k < 32; k += 2)
-              pk[k >> 1] = ptx::pack_bf16(pv[cc + k] * (__uint_as_float(dp[cc + k]) - dd),
-                                          pv[cc + k + 1] * (__uint_as_float(dp[cc + k + 1]) - dd));
+            for (int k = 0; k < 32; k += 2) {  // dS = P o (dP - D), packed (same rounding per lane)
+              const float2 t = ptx::fadd2(make_float2(__uint_as_float(dp[cc + k]), __uint_as_float(dp[cc + k + 1])),
+                                          make_float2(-dd, -dd));
+              const float2 r = ptx::fmul2(make_float2(pv[cc + k], pv[cc + k + 1]), t);
+              pk[k >> 1] = ptx::pack_bf16(r.x, r.y);
+            }
             ptx::tmem_st16(trow + kColDP + k0c + cc / 2, pk);  // dS (bf16 pairs) over dP columns this half read
           }
         }
@@ -716,23 +727,27 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
           if (__any_sync(0xffffffffu, qlo > q0c || qhi < q0c + 63)) {
 #pragma unroll
             for (int k = 0; k < 64; k += 4) {
-              const float4 l4 = *reinterpret_cast<const float4*>(sv + q0c + k);
-              const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+              const float4 l4 = *reinterpret_cast<const float4*>(sv + q0c + k);  // -lse2
+              const float2 x0 = ptx::ffma2(make_float2(pv[k], pv[k + 1]), make_float2(c, c), make_float2(l4.x, l4.y));
+              const float2 x1 = ptx::ffma2(make_float2(pv[k + 2], pv[k + 3]), make_float2(c, c), make_float2(l4.z, l4.w));
+              const float xs[4] = {x0.x, x0.y, x1.x, x1.y};
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
                 const int q = q0c + k + u;
-                const float pe = bwd_ex2(fmaf(pv[k + u], c, lv[u]), k + u);  // lv = -lse2
+                const float pe = bwd_ex2(xs[u], k + u);
                 pv[k + u] = (q >= qlo && q <= qhi) ? pe : 0.f;
               }
             }
           } else {
 #pragma unroll
-            for (int k = 0; k < 64; k += 4) {
+            for (int k = 0; k < 64; k += 4) {  // x = S^T c - lse2, two columns per FFMA2 (same rounding as fmaf)
               const float4 l4 = *reinterpret_cast<const float4*>(sv + q0c + k);
-              pv[k] = bwd_ex2(fmaf(pv[k], c, l4.x), k);
-              pv[k + 1] = bwd_ex2(fmaf(pv[k + 1], c, l4.y), k + 1);
-              pv[k + 2] = bwd_ex2(fmaf(pv[k + 2], c, l4.z), k + 2);
-              pv[k + 3] = bwd_ex2(fmaf(pv[k + 3], c, l4.w), k + 3);
+              const float2 x0 = ptx::ffma2(make_float2(pv[k], pv[k + 1]), make_float2(c, c), make_float2(l4.x, l4.y));
+              const float2 x1 = ptx::ffma2(make_float2(pv[k + 2], pv[k + 3]), make_float2(c, c), make_float2(l4.z, l4.w));
+              pv[k] = bwd_ex2(x0.x, k);
+              pv[k + 1] = bwd_ex2(x0.y, k + 1);
+              pv[k + 2] = bwd_ex2(x1.x, k + 2);
+              pv[k + 3] = bwd_ex2(x1.y, k + 3);
             }
           }
           // P^T -> SMEM (SW128 K-major: key row krow, 16-B unit u at (u ^ (krow & 7)))
@@ -763,9 +778,13 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
               const float4 d4 = *reinterpret_cast<const float4*>(sv + kBM + q0c + cc + k);
               const float dvv[4] = {d4.x, d4.y, d4.z, d4.w};
 #pragma unroll
-              for (int u = 0; u < 4; u += 2)
-                pd[(k + u) >> 1] = ptx::pack_bf16(pv[cc + k + u] * (__uint_as_float(dp[cc + k + u]) + dvv[u]),  // dvv = -D
-                                                  pv[cc + k + u + 1] * (__uint_as_float(dp[cc + k + u + 1]) + dvv[u + 1]));
+              for (int u = 0; u < 4; u += 2) {  // dS^T = P^T o (dP^T - D), packed; dvv = -D
+                const float2 t = ptx::fadd2(
+                    make_float2(__uint_as_float(dp[cc + k + u]), __uint_as_float(dp[cc + k + u + 1])),
+                    make_float2(dvv[u], dvv[u + 1]));
+                const float2 r = ptx::fmul2(make_float2(pv[cc + k + u], pv[cc + k + u + 1]), t);
+                pd[(k + u) >> 1] = ptx::pack_bf16(r.x, r.y);
+              }
             }
             ptx::tmem_st16(trow + kColDP + q0c + cc / 2, pd);  // dS^T over consumed dP^T columns
           }
