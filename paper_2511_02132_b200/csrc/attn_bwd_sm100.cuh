@@ -699,6 +699,7 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
     const float c = p.scale_log2;
     BSchedReader sr;
     uint32_t s_phase = 0, o_phase = 0, blk = 0, pt_phase = 0;
+    ATTN_CYC_DECL()
     while (true) {
       const int4 e = sr.next(ctrl);
       if (!e.w) break;
@@ -707,6 +708,7 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
       const int i0 = dkdv_first_qblock<kCausal>(j);
       for (int hh = 0; hh < p.G; ++hh) {
         for (int i = i0; i < p.nblk; ++i) {
+          ATTN_CYC_START();
           // this block's -lse2 / -D: bulk-copied with Q_i, dO_i into ring stage blk % kStages
           const int rs = (int)(blk % C::kStages);
           ptx::mbar_wait(&ctrl->ring_full[rs], (blk / C::kStages) & 1);
@@ -717,7 +719,9 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
           if (kCausal && i == j) qlo = krow;           // query >= key
           if (i == p.nblk - 1) qhi = p.N - 1 - i * kBM;  // ragged tail
           float pv[64];
+          ATTN_CYC_ADD(0);
           ptx::mbar_wait(&ctrl->s_ready, s_phase);
+          ATTN_CYC_ADD(1);
           ptx::tc_fence_after();
           ptx::tmem_ld64(trow + kColS + q0c, reinterpret_cast<uint32_t*>(pv));   // one wait for 64 columns
           ptx::tc_fence_before();
@@ -750,9 +754,11 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
               pv[k + 3] = bwd_ex2(x1.y, k + 3);
             }
           }
+          ATTN_CYC_ADD(2);
           // P^T -> SMEM (SW128 K-major: key row krow, 16-B unit u at (u ^ (krow & 7)))
           // once dV of the previous block has read the buffer
           ptx::mbar_wait(&ctrl->dv_done, pt_phase ^ 1);
+          ATTN_CYC_ADD(6);
           pt_phase ^= 1;
           {
             uint8_t* rowp = spt + half * (kBM * 128) + krow * 128;
@@ -765,7 +771,9 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
           ptx::fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&ctrl->p_ready);
+          ATTN_CYC_ADD(3);
           ptx::mbar_wait(&ctrl->dp_ready, s_phase);
+          ATTN_CYC_ADD(4);
           s_phase ^= 1;
           ptx::tc_fence_after();
           uint32_t dp[64];
@@ -792,6 +800,8 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
           ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&ctrl->ds_ready);
+          ATTN_CYC_ADD(5);
+          ATTN_CYC_COUNT(7);
         }
       }
       ptx::mbar_wait(&ctrl->o_ready, o_phase);
@@ -823,6 +833,7 @@ __global__ void __launch_bounds__(kThreadsKV, 1)
       }
       ptx::tc_fence_before();
     }
+    ATTN_CYC_WRITE(p.dbg, warp - 4)
   }
   ptx::tc_fence_before();
   __syncthreads();

@@ -1,4 +1,5 @@
-"""Cycle account of the fused backward's elementwise warps (library built with
+"""Cycle account of the backward's dK/dV elementwise warps (the fused kernel for
+d <= 64, the two-pass dK/dV kernel for d > 64) (library built with
 -D ATTN_CYCLES, loaded via ATTN_NUMA_LIB): per (key block, query block) pair,
 the average cycles each elementwise warp spends in each step.  Averaged over
 the 8 elementwise warps of the first 64 CTAs.
@@ -31,6 +32,9 @@ blocks = c[:, :, 7].sum()
 per = c[:, :, :7].sum(axis=(0, 1)) / blocks
 names = ["ring wait + setup", "S wait", "ld S + exps + mask", "dv_done wait + P^T pack/st/arrive",
          "dP wait", "ld dP + dS math + dS^T tmem st", "dk_done wait + dS^T STS + fence + arrive"]
+if d > 64:  # two-pass dK/dV kernel (attn_bwd_sm100.cuh)
+    names = ["ring (vector) wait + setup", "S^T wait", "ld S^T + exps + mask", "P^T pack + STS + fence + arrive",
+             "dP^T wait", "ld dP^T + dS^T math + tmem st", "dv_done wait (P^T buffer free)"]
 print(f"shape B{B} H{Hq}/{Hkv} N{N} d{d} causal={causal}: {blocks / (64 * 8):.0f} blocks per warp")
 for n_, x in zip(names, per):
     print(f"  {n_:32s} {x:8.0f} cycles per block")
